@@ -1,0 +1,78 @@
+"""O-SEL: selective recomputation over the stitched KV, one request (test infrastructure only).
+
+Follows PAPER.md:557-566 step by step (SURVEY.md §8(c) O-SEL), with U the non-PREFIX
+positions and c the check layer (reading R1):
+  1. O-ASM (assemble.py) gives the stitched cache KV_st (bf16 values).
+  2. Layers l < c: the full layer for every p in U over prefix + U, causal ("full attention
+     computation in the first decoder layer"); KV_st[l][U] := fresh.
+  3. Check layer c: K_new, V_new for U (RoPE at p); for HIST/ITEM tokens the Eq. 3 divergence
+     with lambda = 1 (R3) in the R4 fixed point, on K_new/V_new rounded to the bf16 value they
+     would be stored as vs the stitched bf16 value.
+  4. Sel = FORCED u window u topk per class (select.select_sel; R5-R7), or a forced Sel.
+  5. Layers c..L-1 on Sel only: q, k, v at the true positions, KV_st[l][Sel] := (k, v),
+     non-selected tokens keep their stitched state (R9), attention of every selected query
+     over all stitched keys at positions <= its own (R11), O-proj, residual, MLP.
+  6. Logits of the last position (always FORCED: the instruction tail), candidate scores =
+     logits[ID token of the candidate], ranked by score desc, ties -> lower slot (R19).
+"""
+import numpy as np
+
+from .layout import PREFIX, HIST, ITEM
+from .numerics import bf16_to_f32, round_bf16, deviation_fixed
+from .select import select_sel
+
+
+def selective_prefill(m, layout, K_bits, V_bits, r_rev_bp, r_item_bp, check_layer=1,
+                      window=0, forced_sel=None, keep_kv=True, exact_kv=False):
+    """K_bits, V_bits: stitched cache per layer [n][Hk][dh] as bf16 bit patterns (O-ASM), or
+    fp64 values when exact_kv (lossless test mode of the exact-cache invariant)."""
+    s = m.s
+    n, L, c = layout.n, s.n_layers, check_layer
+    cls = layout.cls
+    U = np.array([p for p in range(n) if cls[p] != PREFIX], dtype=np.int64)
+    assert len(U) == 0 or U[0] == n - len(U), "PREFIX must be the leading positions"
+    if exact_kv:
+        K = [np.array(K_bits[l], dtype=np.float64) for l in range(L)]
+        V = [np.array(V_bits[l], dtype=np.float64) for l in range(L)]
+    else:
+        K = [bf16_to_f32(K_bits[l]).astype(np.float64) for l in range(L)]
+        V = [bf16_to_f32(V_bits[l]).astype(np.float64) for l in range(L)]
+
+    x = m.embed(layout.tokens[U])
+    for l in range(c):
+        q, k, v = m.qkv(l, x, U)
+        K[l][U], V[l][U] = k, v
+        o = m.attend(q, U, K[l], V[l])
+        x = m.post(l, x, o)
+
+    # check layer c: deviation of the fresh K/V from the stitched cache (lambda = 1)
+    _, k_new, v_new = m.qkv(c, x, U)
+    D = np.zeros(n, dtype=np.uint64)
+    reuse = np.array([cls[p] in (HIST, ITEM) for p in U])
+    if reuse.any():
+        ur = U[reuse]
+        kb = round_bf16(k_new[reuse]).reshape(len(ur), -1)
+        vb = round_bf16(v_new[reuse]).reshape(len(ur), -1)
+        D[ur] = deviation_fixed(kb, round_bf16(K[c][ur]).reshape(len(ur), -1)) + \
+            deviation_fixed(vb, round_bf16(V[c][ur]).reshape(len(ur), -1))
+    if forced_sel is None:
+        sel = select_sel(cls, D, r_rev_bp, r_item_bp, window)
+    else:
+        sel = np.array(sorted(int(p) for p in forced_sel), dtype=np.int32)
+    row_of = {int(p): i for i, p in enumerate(U)}
+    xs = x[[row_of[int(p)] for p in sel]]
+    sp = sel.astype(np.int64)
+    for l in range(c, L):
+        q, k, v = m.qkv(l, xs, sp)
+        K[l][sp], V[l][sp] = k, v
+        o = m.attend(q, sp, K[l], V[l])
+        xs = m.post(l, xs, o)
+    assert sp[-1] == n - 1, "the last position must be selected (FORCED tail)"
+    logits = m.logits(xs[-1])
+    cand = logits[layout.cand_idtok.astype(np.int64)]
+    rank = sorted(range(len(cand)), key=lambda i: (-cand[i], i))
+    out = {"logits": logits, "cand_scores": cand, "rank": np.array(rank), "sel": sel,
+           "D": D, "x_sel": xs}
+    if keep_kv:
+        out["K"], out["V"] = K, V
+    return out

@@ -1,0 +1,98 @@
+"""Pins of oracle/layout.py and oracle/select.py (not gpu)."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle.layout import decompose_prompt, budget, PREFIX, FORCED, HIST, ITEM
+from oracle.select import importance_scores, select_heavy_hitters, select_sel, sel_count, topk_order
+
+
+def test_layout_worked_example(golden):
+    g = golden("layout_spec68.json")
+    lay = decompose_prompt(np.zeros(g["instruction"], int), np.arange(g["history"][0]),
+                           np.ones(g["history"][0], int), [7], [np.arange(g["items"][0]) + 3],
+                           np.zeros(g["tail"], int))
+    assert lay.seg_start[:3] == g["segment_offsets"] and lay.n == g["total"]
+    assert (lay.cls[:207] == PREFIX).all() and (lay.cls[207:257] == HIST).all() and (lay.cls[257:] == ITEM).all()
+    assert list(lay.src_off[257:260]) == [0, 1, 2] and lay.cand_idtok[0] == 3
+
+
+def test_layout_conservation():
+    rng = np.random.default_rng(0)
+    for _ in range(20):
+        P, H, T = rng.integers(0, 50, 3)
+        lens = rng.integers(1, 30, rng.integers(0, 6))
+        lay = decompose_prompt(np.zeros(P, int), np.arange(H), np.zeros(H, int), list(range(len(lens))),
+                               [np.arange(k) for k in lens], np.zeros(T, int))
+        assert lay.n == P + H + sum(lens) + T
+        assert np.bincount(lay.cls, minlength=4).tolist() == [P, T, H, sum(lens)]
+
+
+def test_budget_examples(golden):
+    g = golden("budget_spec413.json")
+    assert budget(g["r_bp"], g["cached_items"] * g["item_len"]) == g["expected_heavy_hitters"]
+    assert budget(1500, 1280) == 192          # integer basis points, not 0.15f
+    assert budget(10000, 77) == 77 and budget(0, 77) == 0 and budget(1, 1) == 1
+
+
+def test_select_heavy_hitters_spec(golden):
+    for c in golden("topk_spec431.json")["cases"]:
+        assert select_heavy_hitters(c["scores"], c["r_bp"], c["window"], len(c["scores"])) == c["expected"]
+
+
+def test_topk_is_unique_dominating_subset_bruteforce():
+    # brute force over all k-subsets: exactly one subset has every member ahead (score desc,
+    # position asc) of every non-member; it is the oracle's top-k
+    rng = np.random.default_rng(1)
+    for _ in range(30):
+        n = 9
+        sc = rng.integers(0, 4, n).tolist()
+        for k in range(n + 1):
+            top = set(topk_order(sc, range(n))[:k])
+            ok = []
+            for sub in itertools.combinations(range(n), k):
+                s = set(sub)
+                if all((sc[a] > sc[b]) or (sc[a] == sc[b] and a < b) for a in s for b in range(n) if b not in s):
+                    ok.append(s)
+            assert ok == [top]
+
+
+def test_select_sel_classes_nesting_and_bounds():
+    rng = np.random.default_rng(2)
+    cls = np.array([PREFIX] * 5 + [HIST] * 40 + [ITEM] * 60 + [FORCED] * 6, np.uint8)
+    D = rng.integers(0, 1000, len(cls))
+    prev = set()
+    for r in (0, 500, 1500, 3000, 10000):
+        sel = select_sel(cls, D, r, r)
+        assert len(sel) == sel_count(cls, r, r) == 6 + budget(r, 40) + budget(r, 60)
+        assert list(sel) == sorted(sel) and set(range(105, 111)) <= set(sel)
+        assert not any(cls[p] == PREFIX for p in sel)
+        assert prev <= set(sel)                        # nested in r
+        prev = set(sel)
+    assert set(select_sel(cls, D, 10000, 10000)) == set(range(5, 111))   # r = 1 -> all of U
+    assert set(select_sel(cls, D, 0, 0)) == set(range(105, 111))         # r = 0 -> FORCED only
+    # per-class ordering: the chosen history tokens carry the largest D of their class
+    sel = set(select_sel(cls, D, 2000, 0))
+    hs = [p for p in range(5, 45) if p in sel]
+    assert min(D[hs]) >= max(D[[p for p in range(5, 45) if p not in sel]])
+    # window: trailing positions become recomputed, outside the budgets
+    selw = select_sel(cls, D, 0, 0, window=10)
+    assert set(selw) == set(range(101, 111)) and sel_count(cls, 0, 0, 10) == 10
+
+
+def test_importance_scores_reductions_and_brute_force():
+    rng = np.random.default_rng(3)
+    n, m = 64, 32
+    A = rng.random(n)
+    Kn, Kc, Vn, Vc = (rng.standard_normal((n, m)) for _ in range(4))
+    assert np.array_equal(importance_scores(A, Kn, Kc, Vn, Vc, 0.0), A)          # lambda = 0
+    assert np.all(importance_scores(A, Kn, Kn, Vn, Vn, 1.0) == 0)               # vanishing divergence
+    S = importance_scores(A, Kn, Kc, Vn, Vc, 0.5)
+    for i in range(n):
+        t = 0.5 * A[i]
+        for j in range(m):
+            t += 0.5 * (abs(Kn[i, j] - Kc[i, j]) + abs(Vn[i, j] - Vc[i, j]))
+        assert abs(S[i] - t) < 1e-12
+    with pytest.raises(ValueError):
+        importance_scores(A[:-1], Kn, Kc, Vn, Vc, 0.5)
