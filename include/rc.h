@@ -1,0 +1,248 @@
+/* librc -- RcLLM beyond-prefix selective-attention prefill on B200 (sm_100a).
+ *
+ * C-ABI boundary of the hot path named by BASELINE.json north_star / SURVEY.md §8(b).
+ * Paper: "RcLLM: Accelerating Generative Recommendation via Beyond-Prefix KV Caching"
+ * (arxiv 2605.07443), PAPER.md line numbers cited per call.
+ *
+ * Conventions
+ *   - Every function returns rc_status (0 = RC_OK, < 0 = error) and never throws; the message
+ *     of the last error on the calling thread is rc_last_error(). On error there are no
+ *     partial effects (pools, sequences and outputs are left as they were).
+ *   - Device pointers are plain CUDA device addresses on the context's device; host pointers
+ *     are read synchronously before the call returns. rc_stream is a cudaStream_t (NULL =
+ *     legacy default stream). All GPU work is enqueued asynchronously on that stream; device
+ *     outputs are valid once the stream reaches that point.
+ *   - One rc_ctx per (process, device); a context is not thread-safe.
+ *   - bf16 values are raw IEEE bfloat16 bit patterns (uint16), row-major.
+ *   - Token classes: PREFIX = shared system prompt (exact prefix KV, never recomputed),
+ *     FORCED = always recomputed (instruction tail, item misses, window), HIST = history token
+ *     mapped to a prototype, ITEM = candidate-item token.
+ */
+#ifndef RC_H
+#define RC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef int32_t rc_status;
+#define RC_OK 0
+#define RC_E_INVALID (-1)     /* bad argument, shape or state                               */
+#define RC_E_NOMEM (-2)       /* device or pinned-host allocation failed                    */
+#define RC_E_CAPACITY (-3)    /* pool / arena / workspace capacity exceeded                 */
+#define RC_E_NOTFOUND (-4)    /* block id not resident (RC_MISS_ERROR), unknown sequence    */
+#define RC_E_EXISTS (-5)      /* duplicate block id on registration                         */
+#define RC_E_CUDA (-6)        /* CUDA runtime error (message has the CUDA error string)     */
+#define RC_E_PEER (-7)        /* peer pool not attached / not accessible                    */
+#define RC_E_UNSUPPORTED (-8) /* parameter combination not built yet (e.g. lambda != 1)     */
+
+typedef struct rc_ctx rc_ctx;
+typedef uint64_t rc_seq;     /* handle of an assembled request (its stitched KV) */
+typedef void* rc_stream;     /* cudaStream_t */
+
+enum { RC_POOL_ITEM_BF16 = 0, RC_POOL_HIST_INT8 = 1, RC_POOL_PREFIX_BF16 = 2 };
+enum { RC_TOK_PREFIX = 0, RC_TOK_FORCED = 1, RC_TOK_HIST = 2, RC_TOK_ITEM = 3 };
+enum { RC_MISS_ERROR = 0, RC_MISS_RECOMPUTE = 1 };
+
+/* Decoder shape (Llama / Qwen2 family). head_dim in {16, 64, 128}. */
+typedef struct rc_model_desc {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
+  double rope_theta; /* RoPE base (rotate-half pairs) */
+  float rms_eps;
+  int32_t qkv_bias; /* 1: q/k/v projections carry a bias (Qwen2) */
+} rc_model_desc;
+
+/* Model weights: device bf16 pointers in HF layout (nn.Linear weight = [out][in]). The
+ * per-layer members point to host arrays of n_layers device pointers. The library copies
+ * q|k|v into one packed [(H+2H_kv)*d_h][d] matrix and gate|up into [2F][d] (interleaved in
+ * 128-row chunks) at rc_create; the other tensors are used in place and must outlive the ctx. */
+typedef struct rc_weights {
+  const void* embed;      /* [vocab][d]   */
+  const void* final_norm; /* [d]          */
+  const void* lm_head;    /* [vocab][d]   */
+  const void* const* ln1; /* [d]          */
+  const void* const* wq;  /* [H*d_h][d]   */
+  const void* const* wk;  /* [H_kv*d_h][d] */
+  const void* const* wv;  /* [H_kv*d_h][d] */
+  const void* const* bq;  /* [H*d_h] or NULL array when !qkv_bias */
+  const void* const* bk;
+  const void* const* bv;
+  const void* const* wo;  /* [d][H*d_h]   */
+  const void* const* ln2; /* [d]          */
+  const void* const* wg;  /* [F][d]       */
+  const void* const* wu;  /* [F][d]       */
+  const void* const* wd;  /* [d][F]       */
+} rc_weights;
+
+/* Capacities (library-owned HBM, allocated at rc_create). Rows are tokens. */
+typedef struct rc_pool_desc {
+  int64_t item_rows;        /* item pool tokens (bf16), incl. the remote-fetch region      */
+  int64_t remote_rows;      /* of item_rows: tokens reserved for rc_fetch_remote (LRU)      */
+  int64_t hist_rows;        /* prototype rows (int8 + fp32 scales)                          */
+  int64_t prefix_rows;      /* prefix pool tokens (bf16)                                    */
+  int64_t arena_rows;       /* stitched-KV arena tokens (sum of live padded requests)       */
+  int32_t max_seq_len;      /* longest prompt; <= 8192 (R6 key packing)                      */
+  int32_t max_batch_tokens; /* largest sum of n in one rc_selective_prefill call            */
+} rc_pool_desc;
+
+/* One request in decomposed form (output of rc_decompose_prompt; host memory). */
+typedef struct rc_request {
+  int32_t n;                 /* prompt length                                               */
+  const int32_t* token_ids;  /* [n]                                                         */
+  const uint8_t* cls;        /* [n] RC_TOK_*; PREFIX positions must be exactly 0..P-1       */
+  const int64_t* src_id;     /* [n] prototype id (HIST), item id (ITEM), else ignored       */
+  const int32_t* src_off;    /* [n] token offset inside the item block (ITEM), else 0       */
+  uint64_t prefix_id;        /* registered PREFIX block (ignored when P == 0)               */
+  int32_t n_cand;            /* candidates, slot order                                      */
+  const int32_t* cand_idtok; /* [n_cand] ID token of each candidate (its first token, R19)  */
+} rc_request;
+
+/* A prompt as segments: system prompt, history tokens,
+ * candidate item blocks in request order, instruction tail. */
+typedef struct rc_prompt {
+  int32_t prefix_len;
+  const int32_t* prefix_tokens;
+  int32_t n_hist;
+  const int64_t* hist_proto;  /* [n_hist] prototype id of every history token (LSH match)   */
+  const int32_t* hist_tokens; /* [n_hist]                                                    */
+  int32_t n_cand;
+  const int64_t* cand_item;   /* [n_cand]                                                    */
+  const int32_t* cand_len;    /* [n_cand]                                                    */
+  const int32_t* cand_tokens; /* concatenated tokens of all candidates                       */
+  int32_t n_tail;
+  const int32_t* tail_tokens;
+} rc_prompt;
+
+typedef struct rc_prefill_params {
+  int32_t r_rev_bp;           /* recompute ratio of history tokens, basis points (R5)        */
+  int32_t r_item_bp;          /* recompute ratio of item tokens, basis points; 10000 = all   */
+  float lambda;               /* Eq. 3 lambda; must be 1.0 (deviation-only, R3)              */
+  int32_t check_layer;        /* c: layers < c full over U, deviation at c (R1), 0 <= c < L   */
+  int32_t window;             /* last `window` positions always recomputed (R7)              */
+  const int32_t* forced_sel;  /* optional host list: Sel positions per request, concatenated,
+                                 ascending, must contain every FORCED position (test mode)   */
+  const int32_t* forced_sel_off; /* [n_req+1] offsets into forced_sel (with forced_sel)      */
+} rc_prefill_params;
+
+/* ---------------------------------------------------------------- lifecycle */
+rc_status rc_create(const rc_model_desc* m, const rc_weights* w, const rc_pool_desc* p, int32_t device,
+                    rc_ctx** out);
+void rc_destroy(rc_ctx* ctx);
+const char* rc_last_error(void);
+int32_t rc_abi_version(void); /* 1 */
+
+/* Split a prompt into per-position arrays (SPEC.md:62-70 worked example:
+ * 207 + 50 + 87 -> segment offsets 0, 207, 257, total 344). Host only. Capacity `cap`
+ * positions; seg_start gets 2 + n_cand + 1 offsets (prefix, history, items..., tail).
+ * Errors: INVALID (negative length), CAPACITY (n > cap). */
+rc_status rc_decompose_prompt(const rc_prompt* pr, int32_t cap, int32_t* n_out, int32_t* token_ids, uint8_t* cls,
+                              int64_t* src_id, int32_t* src_off, int32_t* seg_start);
+
+/* ---------------------------------------------------------------- offline pools */
+/* Register precomputed KV blocks (the offline artifacts of PAPER.md:384-386, 458) into
+ * library-owned pool pages. kv: DEVICE, layout [n_tok_total][L][2][H_kv][d_h] (bf16 for
+ * ITEM/PREFIX, int8 for HIST), K stored post-RoPE at the block's canonical positions
+ * canon_pos[i] .. canon_pos[i]+n_tokens[i]-1 (R14). scales: DEVICE f32 [n_tok_total][L][2][H_kv]
+ * for HIST (per token/layer/K-V/kv-head, R15), else NULL. HIST blocks are single tokens
+ * (prototypes, n_tokens = 1). PREFIX blocks must have canon_pos = 0. Copies on `stream`;
+ * the caller may free kv/scales after the stream passes this point. All-or-nothing.
+ * Errors: EXISTS (duplicate id), CAPACITY (pool full), INVALID (kind / shape). */
+rc_status rc_pool_register_blocks(rc_ctx* ctx, int32_t kind, int32_t n_blocks, const uint64_t* block_ids,
+                                  const int32_t* n_tokens, const int32_t* canon_pos, const void* kv,
+                                  const float* scales, rc_stream stream);
+/* Resident blocks of a kind (host query). */
+rc_status rc_pool_contains(rc_ctx* ctx, int32_t kind, int32_t n, const uint64_t* block_ids, uint8_t* out);
+
+/* ---------------------------------------------------------------- online path */
+/* Retrieval + alignment (PAPER.md:548-551, 566 steps (i)-(ii)): allocate each request's
+ * stitched KV in the arena, resolve HIST tokens to prototype rows and ITEM tokens to item pool
+ * rows, and enqueue the gather kernel that writes bf16(rot(Delta, deq(pool))) for layers
+ * gather_from..L-1 and the exact PREFIX KV for all layers. Delta = position -
+ * canonical position (may be negative). Item misses: RC_MISS_RECOMPUTE turns their tokens
+ * FORCED; RC_MISS_ERROR fails with NOTFOUND and lists up to *n_missing (in:
+ * capacity, out: count) distinct ids in out_missing. Unknown prototype / prefix -> NOTFOUND.
+ * Errors: INVALID (n > max_seq_len, bad classes), CAPACITY (arena full). */
+rc_status rc_assemble(rc_ctx* ctx, int32_t n_req, const rc_request* reqs, int32_t miss_policy, int32_t gather_from,
+                      rc_seq* out_seqs, uint64_t* out_missing, int32_t* n_missing, rc_stream stream);
+
+/* |Sel| per request for the given parameters (host; fixed by the layout, R5). */
+rc_status rc_sel_count(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,
+                       int32_t* counts);
+
+/* Selective recomputation over a ragged batch:
+ * layers < c over all non-prefix tokens U; Eq. 3 deviation (lambda = 1) at layer c in the R4
+ * fixed point; per-class top-k heavy hitters (R5/R6) + FORCED + window; layers c..L-1 for the
+ * selected tokens only over the whole stitched KV (causal by position, R11), updating the
+ * stitched KV at Sel; LM head on the last position. r_bp = 10000 with no PREFIX is full
+ * prefill. Outputs (DEVICE, caller-allocated, each may be NULL):
+ *   logits      f32 [n_req][vocab]          last-position logits
+ *   cand_scores f32 [sum n_cand]            logits[cand_idtok] (R19), request-major
+ *   sel_pos     i32 [sum |Sel|]             selected positions, ascending per request
+ *   hidden      f32 [sum |Sel|][d]          x_L at Sel (before the final norm, R20)
+ * Errors: INVALID (params, c < gather_from of a sequence, forced_sel malformed),
+ * UNSUPPORTED (lambda != 1), CAPACITY (sum n > max_batch_tokens), NOTFOUND (seq). */
+rc_status rc_selective_prefill(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,
+                               float* logits, float* cand_scores, int32_t* sel_pos, float* hidden,
+                               rc_stream stream);
+
+/* Free the stitched KV of sequences (unknown handles are ignored). */
+void rc_release(rc_ctx* ctx, int32_t n, const rc_seq* seqs);
+
+/* ---------------------------------------------------------------- multi-GPU (§8(e)) */
+/* Export the item pool allocation as a CUDA IPC handle (64 bytes) for peers. */
+rc_status rc_pool_export(rc_ctx* ctx, void* ipc_handle_out, int64_t* pool_rows_out);
+/* Map peers' item pools (one-sided NVLink reads). rank = the peer's index used in
+ * rc_fetch_remote; a handle equal to this context's own export maps loopback. */
+rc_status rc_peer_attach(rc_ctx* ctx, int32_t n_peers, const int32_t* peer_rank, const int32_t* peer_device,
+                         const void* const* ipc_handles, const int64_t* pool_rows);
+/* Pull item blocks from their owners' pools over NVLink into this context's remote-cache
+ * region (LRU, library-owned) and make them resident here (the beyond-paper replacement of
+ * "cache misses are computed on-the-fly"). owner_row = the item's first pool row
+ * on the owner (from the owner's rc_pool_locate). Already-resident ids are skipped.
+ * Errors: PEER (rank not attached), CAPACITY (remote region too small for one call). */
+rc_status rc_fetch_remote(rc_ctx* ctx, int32_t n_items, const uint64_t* item_ids, const int32_t* owner_rank,
+                          const int64_t* owner_row, const int32_t* n_tokens, const int32_t* canon_pos,
+                          rc_stream stream);
+/* First pool row of resident item blocks (-1 if absent), for building fetch requests. */
+rc_status rc_pool_locate(rc_ctx* ctx, int32_t n, const uint64_t* item_ids, int64_t* rows_out);
+
+/* ---------------------------------------------------------------- profiling */
+/* Kernel classes for per-kind timing. */
+enum { RC_K_GEMM = 0, RC_K_ATTN = 1, RC_K_GATHER = 2, RC_K_SELECT = 3, RC_K_SMALL = 4, RC_K_LMHEAD = 5,
+       RC_K_FETCH = 6, RC_K_COUNT = 7 };
+/* Start recording a CUDA event pair around every subsequent librc kernel launch of this ctx. */
+rc_status rc_profile_begin(rc_ctx* ctx);
+/* Synchronize the device, stop recording and report per kind (arrays of n_kinds): summed kernel
+ * time in ms, launch count, algorithmic FLOPs (GEMM: 2MNK; attention: 4 H d_h sum_q (pos_q+1))
+ * and algorithmic bytes (gather: pool reads + stitched writes). */
+rc_status rc_profile_end(rc_ctx* ctx, int32_t n_kinds, double* ms, int64_t* count, double* flops, double* bytes);
+
+/* ---------------------------------------------------------------- diagnostics (tests) */
+/* Stitched KV of one layer of a sequence -> DEVICE bf16 k_out/v_out [n][H_kv][d_h]. */
+rc_status rc_seq_read_kv(rc_ctx* ctx, rc_seq seq, int32_t layer, void* k_out, void* v_out, rc_stream stream);
+/* K5+K6 unit path on given bf16 operands (DEVICE): D[i] = sum |a - b| in the R4 fixed point
+ * over `width` elements of K and V, then the selection of rc_selective_prefill for one request
+ * whose U rows are these n_u tokens (classes cls, positions P..P+n_u-1). Outputs: dev_out
+ * u64 [n_u], sel_out i32 [count]. */
+rc_status rc_diag_deviation_select(int32_t n_u, int32_t width, const void* k_new, const void* k_st,
+                                   const void* v_new, const void* v_st, const uint8_t* cls_host, int32_t prefix_len,
+                                   int32_t r_rev_bp, int32_t r_item_bp, int32_t window, uint64_t* dev_out,
+                                   int32_t* sel_out, int32_t* n_sel_out, rc_stream stream);
+/* The tcgen05 GEMM on its own: C f32 [M][N] = A bf16 [M][K] * B bf16 [N][K]^T (DEVICE). */
+rc_status rc_diag_gemm(int32_t M, int32_t N, int32_t K, const void* A, const void* B, float* C, int32_t bn,
+                       rc_stream stream);
+/* Kernel launches issued by this context since creation (every librc kernel counts). */
+int64_t rc_launch_count(rc_ctx* ctx);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* RC_H */

@@ -1,0 +1,244 @@
+"""Thin Python face of librc (same names as include/rc.h, argument marshalling only).
+
+PyTorch provides device memory and streams; every computation of the hot path happens in
+librc's sm_100a kernels. Nothing here imports oracle/.
+"""
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as R
+from ._lib import check, lib, np_ptr
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _dptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _ptr_array(tensors):
+    arr = (C.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    return C.cast(arr, R.PP), arr
+
+
+class RcContext:
+    """rc_create/rc_destroy around one device. `weights`: rcgen naming, bf16 CUDA tensors."""
+
+    def __init__(self, shape, weights, item_rows, hist_rows, prefix_rows, arena_rows, max_seq_len, max_batch_tokens,
+                 remote_rows=0, device=0):
+        lib()
+        self.shape = shape
+        self.device = device
+        self._keep = [weights]
+        md = R.ModelDesc(shape.n_layers, shape.d_model, shape.n_heads, shape.n_kv_heads, shape.head_dim, shape.d_ff,
+                         shape.vocab, float(shape.rope_theta), float(shape.rms_eps), int(shape.qkv_bias))
+        w = R.Weights()
+        w.embed, w.final_norm, w.lm_head = (weights[k].data_ptr() for k in ("embed", "norm", "lm_head"))
+        for name in ("ln1", "wq", "wk", "wv", "wo", "ln2", "wg", "wu", "wd") + (("bq", "bk", "bv") if shape.qkv_bias else ()):
+            p, arr = _ptr_array([lw[name] for lw in weights["layers"]])
+            self._keep.append(arr)
+            setattr(w, name, p)
+        pd = R.PoolDesc(item_rows, remote_rows, hist_rows, prefix_rows, arena_rows, max_seq_len, max_batch_tokens)
+        out = C.c_void_p()
+        check(lib().rc_create(C.byref(md), C.byref(w), C.byref(pd), device, C.byref(out)))
+        self.ctx = out
+        self.max_batch_tokens = max_batch_tokens
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().rc_destroy(self.ctx)
+            self.ctx = None
+
+    __del__ = close
+
+    # ------------------------------------------------------------------ pools
+    def pool_register_blocks(self, kind, ids, n_tokens, canon_pos, kv, scales=None, stream=None):
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        nt = np.ascontiguousarray(n_tokens, dtype=np.int32)
+        cp = np.ascontiguousarray(canon_pos, dtype=np.int32)
+        assert kv.is_cuda and kv.is_contiguous()
+        check(lib().rc_pool_register_blocks(self.ctx, kind, len(ids), np_ptr(ids, C.c_uint64), np_ptr(nt, C.c_int32),
+                                            np_ptr(cp, C.c_int32), _dptr(kv), _dptr(scales), _stream(stream)))
+
+    def pool_contains(self, kind, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        out = np.zeros(len(ids), np.uint8)
+        check(lib().rc_pool_contains(self.ctx, kind, len(ids), np_ptr(ids, C.c_uint64), np_ptr(out, C.c_uint8)))
+        return out.astype(bool)
+
+    def pool_locate(self, ids):
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        out = np.zeros(len(ids), np.int64)
+        check(lib().rc_pool_locate(self.ctx, len(ids), np_ptr(ids, C.c_uint64), np_ptr(out, C.c_int64)))
+        return out
+
+    # ------------------------------------------------------------------ requests
+    @staticmethod
+    def decompose_prompt(prefix_tokens, hist_proto, hist_tokens, cand_item, cand_tokens, tail_tokens):
+        pt = np.ascontiguousarray(prefix_tokens, np.int32)
+        hp = np.ascontiguousarray(hist_proto, np.int64)
+        ht = np.ascontiguousarray(hist_tokens, np.int32)
+        ci = np.ascontiguousarray(cand_item, np.int64)
+        cl = np.ascontiguousarray([len(t) for t in cand_tokens], np.int32)
+        ct = np.ascontiguousarray(np.concatenate([np.asarray(t, np.int32) for t in cand_tokens]) if len(cand_tokens)
+                                  else np.zeros(0, np.int32))
+        tt = np.ascontiguousarray(tail_tokens, np.int32)
+        pr = R.Prompt(len(pt), np_ptr(pt, C.c_int32), len(hp), np_ptr(hp, C.c_int64), np_ptr(ht, C.c_int32), len(ci),
+                      np_ptr(ci, C.c_int64), np_ptr(cl, C.c_int32), np_ptr(ct, C.c_int32), len(tt), np_ptr(tt, C.c_int32))
+        cap = len(pt) + len(ht) + int(cl.sum()) + len(tt)
+        tok = np.zeros(cap, np.int32); cls = np.zeros(cap, np.uint8); sid = np.zeros(cap, np.int64)
+        soff = np.zeros(cap, np.int32); seg = np.zeros(3 + len(ci), np.int32)
+        n = C.c_int32()
+        check(lib().rc_decompose_prompt(C.byref(pr), cap, C.byref(n), np_ptr(tok, C.c_int32), np_ptr(cls, C.c_uint8),
+                                        np_ptr(sid, C.c_int64), np_ptr(soff, C.c_int32), np_ptr(seg, C.c_int32)))
+        idtok = np.array([int(t[0]) for t in cand_tokens], np.int32)
+        return dict(tokens=tok[:n.value], cls=cls[:n.value], src_id=sid[:n.value], src_off=soff[:n.value],
+                    seg_start=seg, cand_idtok=idtok)
+
+    def assemble(self, layouts, prefix_id=0, miss_policy=R.RC_MISS_RECOMPUTE, gather_from=1, stream=None):
+        """layouts: dicts with tokens, cls, src_id, src_off, cand_idtok (host arrays)."""
+        n = len(layouts)
+        reqs = (R.Request * n)()
+        keep = []
+        for i, lay in enumerate(layouts):
+            arrs = [np.ascontiguousarray(lay["tokens"], np.int32), np.ascontiguousarray(lay["cls"], np.uint8),
+                    np.ascontiguousarray(lay["src_id"], np.int64), np.ascontiguousarray(lay["src_off"], np.int32),
+                    np.ascontiguousarray(lay["cand_idtok"], np.int32)]
+            keep.append(arrs)
+            reqs[i] = R.Request(len(arrs[0]), np_ptr(arrs[0], C.c_int32), np_ptr(arrs[1], C.c_uint8),
+                                np_ptr(arrs[2], C.c_int64), np_ptr(arrs[3], C.c_int32), prefix_id, len(arrs[4]),
+                                np_ptr(arrs[4], C.c_int32))
+        seqs = np.zeros(n, np.uint64)
+        missing = np.zeros(4096, np.uint64)
+        nm = C.c_int32(len(missing))
+        code = lib().rc_assemble(self.ctx, n, reqs, miss_policy, gather_from, np_ptr(seqs, C.c_uint64),
+                                 np_ptr(missing, C.c_uint64), C.byref(nm), _stream(stream))
+        self.last_missing = missing[:min(nm.value, len(missing))].copy()
+        check(code)
+        return seqs
+
+    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0):
+        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None)
+        keep = None
+        if forced_sel is not None:
+            off = np.zeros(len(forced_sel) + 1, np.int32)
+            off[1:] = np.cumsum([len(s) for s in forced_sel])
+            flat = np.ascontiguousarray(np.concatenate([np.asarray(s, np.int32) for s in forced_sel]), np.int32)
+            prm.forced_sel = np_ptr(flat, C.c_int32)
+            prm.forced_sel_off = np_ptr(off, C.c_int32)
+            keep = (flat, off)
+        return prm, keep
+
+    def sel_count(self, seqs, r_rev_bp, r_item_bp, check_layer=1, window=0):
+        seqs = np.ascontiguousarray(seqs, np.uint64)
+        prm, _ = self._params(r_rev_bp, r_item_bp, check_layer, window, None)
+        out = np.zeros(len(seqs), np.int32)
+        check(lib().rc_sel_count(self.ctx, len(seqs), np_ptr(seqs, C.c_uint64), C.byref(prm), np_ptr(out, C.c_int32)))
+        return out
+
+    def selective_prefill(self, seqs, r_rev_bp, r_item_bp, check_layer=1, window=0, forced_sel=None, lam=1.0,
+                          logits=True, cand_scores=True, sel_pos=True, hidden=False, n_cand=None, out=None,
+                          stream=None):
+        """Returns dict of CUDA tensors (logits, cand_scores, sel_pos, hidden) as requested. `out`
+        may hold preallocated tensors with the same keys (reused; no allocation)."""
+        seqs = np.ascontiguousarray(seqs, np.uint64)
+        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam)
+        dev = torch.device("cuda", self.device)
+        res = dict(out) if out else {}
+        if (sel_pos or hidden) and ("sel_pos" not in res and "hidden" not in res):
+            cnt = self.sel_count(seqs, r_rev_bp, r_item_bp, check_layer, window)
+            S = int(cnt.sum())
+            res["sel_off"] = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+        if logits and "logits" not in res:
+            res["logits"] = torch.empty((len(seqs), self.shape.vocab), dtype=torch.float32, device=dev)
+        if cand_scores and "cand_scores" not in res:
+            res["cand_scores"] = torch.empty((int(n_cand),), dtype=torch.float32, device=dev)
+        if sel_pos and "sel_pos" not in res:
+            res["sel_pos"] = torch.empty((S,), dtype=torch.int32, device=dev)
+        if hidden and "hidden" not in res:
+            res["hidden"] = torch.empty((S, self.shape.d_model), dtype=torch.float32, device=dev)
+        check(lib().rc_selective_prefill(self.ctx, len(seqs), np_ptr(seqs, C.c_uint64), C.byref(prm),
+                                         _dptr(res.get("logits") if logits else None),
+                                         _dptr(res.get("cand_scores") if cand_scores else None),
+                                         _dptr(res.get("sel_pos") if sel_pos else None),
+                                         _dptr(res.get("hidden") if hidden else None), _stream(stream)))
+        return res
+
+    def read_kv(self, seq, layer, n, stream=None):
+        s = self.shape
+        dev = torch.device("cuda", self.device)
+        k = torch.empty((n, s.n_kv_heads, s.head_dim), dtype=torch.int16, device=dev)
+        v = torch.empty_like(k)
+        check(lib().rc_seq_read_kv(self.ctx, int(seq), layer, _dptr(k), _dptr(v), _stream(stream)))
+        return k, v
+
+    def release(self, seqs):
+        seqs = np.ascontiguousarray(seqs, np.uint64)
+        lib().rc_release(self.ctx, len(seqs), np_ptr(seqs, C.c_uint64))
+
+    def launch_count(self):
+        return int(lib().rc_launch_count(self.ctx))
+
+    def profile_begin(self):
+        check(lib().rc_profile_begin(self.ctx))
+
+    def profile_end(self):
+        """-> {kind: dict(ms, launches, flops, bytes)} summed over the profiled launches."""
+        n = len(R.KINDS)
+        ms = (C.c_double * n)(); cnt = (C.c_int64 * n)(); fl = (C.c_double * n)(); by = (C.c_double * n)()
+        check(lib().rc_profile_end(self.ctx, n, ms, cnt, fl, by))
+        return {k: dict(ms=ms[i], launches=cnt[i], flops=fl[i], bytes=by[i]) for i, k in enumerate(R.KINDS)}
+
+    # ------------------------------------------------------------------ multi-GPU
+    def pool_export(self):
+        h = (C.c_uint8 * 64)()
+        rows = C.c_int64()
+        check(lib().rc_pool_export(self.ctx, C.cast(h, C.c_void_p), C.byref(rows)))
+        return bytes(h), rows.value
+
+    def peer_attach(self, ranks, devices, handles, rows):
+        n = len(ranks)
+        r = np.ascontiguousarray(ranks, np.int32)
+        d = np.ascontiguousarray(devices, np.int32)
+        bufs = [(C.c_uint8 * 64).from_buffer_copy(h) for h in handles]
+        hp = (C.c_void_p * n)(*[C.addressof(b) for b in bufs])
+        rw = np.ascontiguousarray(rows, np.int64)
+        check(lib().rc_peer_attach(self.ctx, n, np_ptr(r, C.c_int32), np_ptr(d, C.c_int32), C.cast(hp, R.PP),
+                                   np_ptr(rw, C.c_int64)))
+
+    def fetch_remote(self, item_ids, owner_rank, owner_row, n_tokens, canon_pos, stream=None):
+        ids = np.ascontiguousarray(item_ids, np.uint64)
+        o = np.ascontiguousarray(owner_rank, np.int32)
+        orow = np.ascontiguousarray(owner_row, np.int64)
+        nt = np.ascontiguousarray(n_tokens, np.int32)
+        cp = np.ascontiguousarray(canon_pos, np.int32)
+        check(lib().rc_fetch_remote(self.ctx, len(ids), np_ptr(ids, C.c_uint64), np_ptr(o, C.c_int32),
+                                    np_ptr(orow, C.c_int64), np_ptr(nt, C.c_int32), np_ptr(cp, C.c_int32),
+                                    _stream(stream)))
+
+
+def diag_gemm(A, B, bn=256, stream=None):
+    M, K = A.shape
+    N = B.shape[0]
+    Cm = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    check(lib().rc_diag_gemm(M, N, K, _dptr(A), _dptr(B), _dptr(Cm), bn, _stream(stream)))
+    return Cm
+
+
+def diag_deviation_select(k_new, k_st, v_new, v_st, cls, prefix_len, r_rev_bp, r_item_bp, window=0, stream=None):
+    """bf16 (int16-viewed) CUDA tensors [n_u][width] -> (D uint64 numpy, Sel positions numpy)."""
+    n_u, width = k_new.shape
+    dev = torch.empty((n_u,), dtype=torch.int64, device=k_new.device)
+    sel = torch.empty((n_u + 1,), dtype=torch.int32, device=k_new.device)
+    cls = np.ascontiguousarray(cls, np.uint8)
+    ns = C.c_int32()
+    check(lib().rc_diag_deviation_select(n_u, width, _dptr(k_new), _dptr(k_st), _dptr(v_new), _dptr(v_st),
+                                         np_ptr(cls, C.c_uint8), prefix_len, r_rev_bp, r_item_bp, window, _dptr(dev),
+                                         _dptr(sel), C.byref(ns), _stream(stream)))
+    return dev.cpu().numpy().view(np.uint64), sel[:ns.value].cpu().numpy()

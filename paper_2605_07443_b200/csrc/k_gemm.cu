@@ -1,0 +1,352 @@
+// K3: persistent warp-specialised tcgen05 GEMM for every dense projection of the hot path,
+// with the per-row work fused into its epilogue.
+//
+//   C[M][N] = A[M][K] * B[N][K]^T    (A = activations, B = weight rows; both bf16, K-major)
+//
+// Roles (256 threads, 1 CTA/SM, grid = min(tiles, #SM), static round-robin tile order):
+//   warp 0      TMA producer: A 128x64 and B BNx64 boxes, SWIZZLE_128B, STAGES-deep mbarrier ring
+//   warp 1      MMA issuer (one thread): tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16
+//   warp 2      TMEM allocator (2 x BN fp32 columns = double-buffered accumulator)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b (thread <-> accumulator row), fused epilogue op
+// The epilogue of tile i overlaps the MMAs of tile i+1 (two TMEM accumulator stages).
+#include <mutex>
+
+#include "common.cuh"
+#include "rc_internal.h"
+
+namespace rc {
+
+namespace {
+constexpr int BM = 128, BK = 64;
+constexpr int GROUP_M = 16;  // raster: GROUP_M m-tiles share a sweep over n (L2 reuse of A and B)
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = GROUP_M * num_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  const int gm = min(GROUP_M, num_m - first_m);
+  const int r = t - g * per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+__device__ __forceinline__ void st_bf16x16(uint16_t* dst, const float* v) {
+  uint4 a, b;
+  a.x = pack_bf2(v[0], v[1]); a.y = pack_bf2(v[2], v[3]); a.z = pack_bf2(v[4], v[5]); a.w = pack_bf2(v[6], v[7]);
+  b.x = pack_bf2(v[8], v[9]); b.y = pack_bf2(v[10], v[11]); b.z = pack_bf2(v[12], v[13]); b.w = pack_bf2(v[14], v[15]);
+  reinterpret_cast<uint4*>(dst)[0] = a;
+  reinterpret_cast<uint4*>(dst)[1] = b;
+}
+template <int CW>
+__device__ __forceinline__ void st_bf16xCW(uint16_t* dst, const float* v) {
+  if constexpr (CW == 16) {
+    st_bf16x16(dst, v);
+  } else {
+    uint4 a;
+    a.x = pack_bf2(v[0], v[1]); a.y = pack_bf2(v[2], v[3]); a.z = pack_bf2(v[4], v[5]); a.w = pack_bf2(v[6], v[7]);
+    reinterpret_cast<uint4*>(dst)[0] = a;
+  }
+}
+template <int CW>
+__device__ __forceinline__ void tmem_ldCW(uint32_t taddr, float* v) {
+  if constexpr (CW == 16) tmem_ld16(taddr, v); else tmem_ld8(taddr, v);
+}
+__device__ __forceinline__ void add_bias(float* v, const uint16_t* b, int n) {
+  if (b)
+#pragma unroll
+    for (int j = 0; j < n; ++j) v[j] += bf2f(b[j]);
+}
+// Fused QKV / deviation epilogue over the heads of one tile (templated on the RoPE chunk width).
+template <int BN, int CW, bool DEV>
+__device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool row_ok, int row, const EpiArgs& ep,
+                                          unsigned long long& dev_acc) {
+  const int dh = ep.head_dim;
+  const int H = DEV ? 0 : ep.n_heads;
+  const int Hk = ep.n_kv_heads;
+  int pos = 0, drow = 0;
+  if (row_ok) { pos = ep.pos[row]; drow = ep.dst_row[row]; }
+  const float* cs_row = ep.rope_cos + static_cast<int64_t>(pos + ep.rope_zero) * (dh / 2);
+  const float* sn_row = ep.rope_sin + static_cast<int64_t>(pos + ep.rope_zero) * (dh / 2);
+  const int heads_in_tile = BN / dh;
+  for (int hi = 0; hi < heads_in_tile; ++hi) {
+    const int hh = n0 / dh + hi;  // head index in the packed output
+    if (hh * dh >= N) break;
+    const int col0 = hi * dh;
+    const bool is_q = hh < H;
+    const bool is_k = !is_q && hh < H + Hk;
+    const uint16_t* bias = ep.bias ? ep.bias + hh * dh : nullptr;
+    if (is_q || is_k) {
+      uint16_t* dst;
+      const uint16_t* st = nullptr;
+      if (is_q) dst = ep.q_out + static_cast<int64_t>(row) * ep.q_ld + hh * dh;
+      else {
+        const int64_t off = static_cast<int64_t>(hh - H) * ep.head_stride + static_cast<int64_t>(drow) * dh;
+        dst = ep.arena_k + off;
+        st = ep.arena_k + off;
+      }
+      for (int c = 0; c < dh / 2; c += CW) {
+        float lo[CW], hv[CW];
+        tmem_ldCW<CW>(taddr + col0 + c, lo);
+        tmem_ldCW<CW>(taddr + col0 + dh / 2 + c, hv);
+        if (!row_ok) continue;
+        if (bias) { add_bias(lo, bias + c, CW); add_bias(hv, bias + dh / 2 + c, CW); }
+        float y0[CW], y1[CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          const float cc = cs_row[c + j], ss = sn_row[c + j];
+          y0[j] = __fsub_rn(__fmul_rn(lo[j], cc), __fmul_rn(hv[j], ss));
+          y1[j] = __fadd_rn(__fmul_rn(hv[j], cc), __fmul_rn(lo[j], ss));
+        }
+        if constexpr (DEV) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            dev_acc += dev_term(y0[j], st[c + j]);
+            dev_acc += dev_term(y1[j], st[dh / 2 + c + j]);
+          }
+        } else {
+          st_bf16xCW<CW>(dst + c, y0);
+          st_bf16xCW<CW>(dst + dh / 2 + c, y1);
+        }
+      }
+    } else {  // V head: no rotation
+      const int64_t off = static_cast<int64_t>(hh - H - Hk) * ep.head_stride + static_cast<int64_t>(drow) * dh;
+      uint16_t* dst = ep.arena_v + off;
+      for (int c = 0; c < dh; c += CW) {
+        float v[CW];
+        tmem_ldCW<CW>(taddr + col0 + c, v);
+        if (!row_ok) continue;
+        if (bias) add_bias(v, bias + c, CW);
+        if constexpr (DEV) {
+#pragma unroll
+          for (int j = 0; j < CW; ++j) dev_acc += dev_term(v[j], dst[c + j]);
+        } else {
+          st_bf16xCW<CW>(dst + c, v);
+        }
+      }
+    }
+  }
+}
+
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, int M, int N, int lane_base,
+                                              const EpiArgs& ep) {
+  const int row = m0 + lane_base + (threadIdx.x & 31);
+  const bool row_ok = row < M;
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_F32 || EPI == EPI_ADD_F32) {
+    for (int c = 0; c < BN; c += 16) {
+      if (n0 + c >= N) break;  // uniform
+      float v[16];
+      tmem_ld16(taddr + c, v);
+      if (!row_ok) continue;
+      if (n0 + c + 16 > N) {  // ragged N tail (N % 16 != 0): element stores
+        const int nv = N - n0 - c;
+        for (int j = 0; j < nv; ++j) {
+          float val = v[j] + ((EPI == EPI_BF16 && ep.bias) ? bf2f(ep.bias[n0 + c + j]) : 0.f);
+          const int64_t idx = static_cast<int64_t>(row) * ep.ldo + n0 + c + j;
+          if constexpr (EPI == EPI_BF16) static_cast<uint16_t*>(ep.out)[idx] = f2bf(val);
+          else if constexpr (EPI == EPI_F32) static_cast<float*>(ep.out)[idx] = val;
+          else static_cast<float*>(ep.out)[idx] += val;
+        }
+        continue;
+      }
+      if constexpr (EPI == EPI_BF16) {
+        if (ep.bias) add_bias(v, ep.bias + n0 + c, 16);
+        st_bf16x16(static_cast<uint16_t*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + n0 + c, v);
+      } else {
+        float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + n0 + c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          if constexpr (EPI == EPI_ADD_F32) {
+            const float4 x = o[j];
+            w.x += x.x; w.y += x.y; w.z += x.z; w.w += x.w;
+          }
+          o[j] = w;
+        }
+      }
+    }
+  } else if constexpr (EPI == EPI_SWIGLU) {
+    static_assert(BN == 256, "SwiGLU epilogue needs [128 gate | 128 up] tiles");
+    for (int c = 0; c < 128; c += 16) {
+      float g[16], u[16];
+      tmem_ld16(taddr + c, g);
+      tmem_ld16(taddr + 128 + c, u);
+      if (!row_ok) continue;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) g[j] = g[j] / (1.0f + __expf(-g[j])) * u[j];
+      st_bf16x16(static_cast<uint16_t*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + n0 / 2 + c, g);
+    }
+  } else {
+    constexpr bool DEV = (EPI == EPI_DEV);
+    unsigned long long acc = 0;
+    if (ep.head_dim >= 32) epi_heads<BN, 16, DEV>(taddr, n0, N, row_ok, row, ep, acc);
+    else epi_heads<BN, 8, DEV>(taddr, n0, N, row_ok, row, ep, acc);
+    if constexpr (DEV) {
+      if (row_ok && ep.row_reuse[row]) atomicAdd(ep.dev_out + row, acc);
+    }
+  }
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+           const EpiArgs ep) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
+  const int nk = (K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int mb, nb; tile_coords(t, num_m, num_n, mb, nb);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int stage = 0; uint32_t phase = 0; int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue warps
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      int mb, nb; tile_coords(t, num_m, num_n, mb, nb);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      epilogue_tile<BN, EPI>(taddr, mb * BM, nb * BN, M, N, q * 32, ep);
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+template <int BN, int EPI>
+cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, int M, int N, int K, const EpiArgs& ep, int num_sms,
+                       cudaStream_t s) {
+  using C = GemmCfg<BN>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  k_gemm<BN, EPI><<<grid, 256, C::SMEM, s>>>(*a, *b, M, N, K, ep);
+  return cudaGetLastError();
+}
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+}  // namespace
+
+int gemm_box_rows_b(int bn) { return bn; }
+
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                       uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, int M, int N, int K, int bn, int epi,
+                        const EpiArgs& ep, int num_sms, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+#define RC_GEMM_CASE(BN_, E_) \
+  if (bn == BN_ && epi == E_) return launch_one<BN_, E_>(a, b, M, N, K, ep, num_sms, s);
+  RC_GEMM_CASE(256, EPI_BF16) RC_GEMM_CASE(256, EPI_F32) RC_GEMM_CASE(256, EPI_ADD_F32)
+  RC_GEMM_CASE(256, EPI_SWIGLU) RC_GEMM_CASE(256, EPI_QKV) RC_GEMM_CASE(256, EPI_DEV)
+  RC_GEMM_CASE(128, EPI_BF16) RC_GEMM_CASE(128, EPI_F32) RC_GEMM_CASE(128, EPI_ADD_F32)
+  RC_GEMM_CASE(128, EPI_QKV) RC_GEMM_CASE(128, EPI_DEV)
+#undef RC_GEMM_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace rc

@@ -1,0 +1,336 @@
+// Small bandwidth / latency-bound kernels of the hot path:
+//   embed       a2: x[U] = E[t]  (fp32 residual stream, R22)
+//   rmsnorm     a2/a5/a7/a8: bf16(x / sqrt(mean(x^2) + eps) * g)
+//   select      a4 (K6): per-request, per-class top-k by the R6 key via 8-bit radix select,
+//               union FORCED and window, compaction in position order
+//   gather_rows a4: x_sel = x[Sel]
+//   cand_scores a8: score_c = logits[idtok_c] (R19)
+// plus pool registration transposes, the NVLink / loopback fetch copy and a diagnostic reader.
+#include "common.cuh"
+#include "rc_internal.h"
+
+namespace rc {
+namespace {
+
+enum { CLS_PREFIX = 0, CLS_FORCED = 1, CLS_HIST = 2, CLS_ITEM = 3 };
+
+__global__ void k_embed(const uint16_t* __restrict__ emb, const int32_t* __restrict__ tok, int32_t rows, int32_t d,
+                        float* __restrict__ x) {
+  const int64_t n8 = static_cast<int64_t>(rows) * (d / 8);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / (d / 8);
+    const int c = static_cast<int>(i % (d / 8)) * 8;
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(emb + static_cast<int64_t>(tok[r]) * d + c));
+    float4 a = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                           __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+    float4 b = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u),
+                           __uint_as_float(u.w << 16), __uint_as_float(u.w & 0xFFFF0000u));
+    float4* dst = reinterpret_cast<float4*>(x + r * d + c);
+    dst[0] = a;
+    dst[1] = b;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, const int32_t* __restrict__ row_idx,
+                                                 int32_t d, const uint16_t* __restrict__ g, float eps,
+                                                 uint16_t* __restrict__ out) {
+  __shared__ float red[8];
+  const int r = blockIdx.x;
+  const int64_t src = row_idx ? row_idx[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = xr[i];
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffff, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / d + eps);
+  uint2* orow = reinterpret_cast<uint2*>(out + static_cast<int64_t>(r) * d);
+  const uint2* grow = reinterpret_cast<const uint2*>(g);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = xr[i];
+    const uint2 gg = __ldg(&grow[i]);
+    uint2 o;
+    o.x = pack_bf2(v.x * inv * __uint_as_float(gg.x << 16), v.y * inv * __uint_as_float(gg.x & 0xFFFF0000u));
+    o.y = pack_bf2(v.z * inv * __uint_as_float(gg.y << 16), v.w * inv * __uint_as_float(gg.y & 0xFFFF0000u));
+    orow[i] = o;
+  }
+}
+
+__global__ void k_gather_rows(const float* __restrict__ src, const int32_t* __restrict__ idx, int32_t rows, int32_t d,
+                              float* __restrict__ dst) {
+  const int64_t n4 = static_cast<int64_t>(rows) * (d / 4);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / (d / 4);
+    const int c = static_cast<int>(i % (d / 4));
+    reinterpret_cast<float4*>(dst + r * d)[c] = reinterpret_cast<const float4*>(src + static_cast<int64_t>(idx[r]) * d)[c];
+  }
+}
+
+// ----------------------------------------------------------------------------- K6 selection
+constexpr int SEL_THREADS = 1024;
+constexpr int SEL_MAX_U = 8192;
+
+__device__ __forceinline__ unsigned long long sel_key(unsigned long long dev, int pos) {
+  return (dev << 13) | static_cast<unsigned long long>(8191 - pos);  // R6: D desc, then pos asc
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
+  __shared__ uint8_t flag[SEL_MAX_U];
+  __shared__ uint8_t cls[SEL_MAX_U];
+  __shared__ int hist[256];
+  __shared__ int sh_digit, sh_krem, sh_members;
+  __shared__ int scan[SEL_THREADS];
+  const int4 rq = a.req[blockIdx.x];
+  const int4 rq2 = a.req2[blockIdx.x];
+  const int u_off = rq.x, u_cnt = rq.y, sel_off = rq.z, n = rq.w;
+  const int P = n - u_cnt;
+  const int window = rq2.w;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < u_cnt; i += SEL_THREADS) {
+    const int pos = P + i;
+    int c = a.ucls[u_off + i];
+    const bool in_win = window > 0 && pos >= n - window;
+    if (in_win) c = CLS_FORCED;
+    cls[i] = static_cast<uint8_t>(c);
+    flag[i] = (c == CLS_FORCED) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    const int want = pass == 0 ? CLS_HIST : CLS_ITEM;
+    const int k = pass == 0 ? rq2.x : rq2.y;
+    if (tid == 0) sh_members = 0;
+    __syncthreads();
+    int cnt = 0;
+    for (int i = tid; i < u_cnt; i += SEL_THREADS) cnt += (cls[i] == want);
+    atomicAdd(&sh_members, cnt);
+    __syncthreads();
+    const int members = sh_members;
+    if (k <= 0) continue;
+    unsigned long long thr = 0;
+    if (k < members) {
+      unsigned long long prefix = 0, mask = 0;
+      if (tid == 0) sh_krem = k;
+      for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int i = tid; i < 256; i += SEL_THREADS) hist[i] = 0;
+        __syncthreads();
+        for (int i = tid; i < u_cnt; i += SEL_THREADS) {
+          if (cls[i] != want) continue;
+          const unsigned long long key = sel_key(a.dev[u_off + i], P + i);
+          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          int c = 0, krem = sh_krem, dgt = 0;
+          for (int d = 255; d >= 0; --d) {
+            if (c + hist[d] >= krem) { dgt = d; krem -= c; break; }
+            c += hist[d];
+          }
+          sh_digit = dgt;
+          sh_krem = krem;
+        }
+        __syncthreads();
+        prefix |= static_cast<unsigned long long>(sh_digit) << shift;
+        mask |= 255ull << shift;
+        __syncthreads();
+      }
+      thr = prefix;  // keys are unique: exactly k member keys are >= the k-th largest
+    }
+    for (int i = tid; i < u_cnt; i += SEL_THREADS)
+      if (cls[i] == want && sel_key(a.dev[u_off + i], P + i) >= thr) flag[i] = 1;
+    __syncthreads();
+  }
+  // compaction in position order
+  const int per = (u_cnt + SEL_THREADS - 1) / SEL_THREADS;
+  const int b = tid * per, e = min(u_cnt, b + per);
+  int cnt = 0;
+  for (int i = b; i < e; ++i) cnt += flag[i];
+  scan[tid] = cnt;
+  __syncthreads();
+  for (int o = 1; o < SEL_THREADS; o <<= 1) {
+    const int v = tid >= o ? scan[tid - o] : 0;
+    __syncthreads();
+    scan[tid] += v;
+    __syncthreads();
+  }
+  int w = sel_off + scan[tid] - cnt;
+  for (int i = b; i < e; ++i) {
+    if (!flag[i]) continue;
+    a.sel_pos[w] = P + i;
+    a.sel_dst[w] = rq2.z + P + i;
+    a.sel_urow[w] = u_off + i;
+    ++w;
+  }
+}
+
+__global__ void k_cand_scores(const float* logits, int64_t vocab, const int32_t* cand_req, const int32_t* idtok, int32_t n,
+                              float* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = logits[static_cast<int64_t>(cand_req[i]) * vocab + idtok[i]];
+}
+
+// [n_tok][L][2][Hk][dh] -> [L][2][Hk][dst_rows][dh] at rows dst_row0 + t (16-byte chunks)
+__global__ void k_pool_transpose(const uint8_t* __restrict__ src, int eb, int32_t n_tok, int32_t L, int32_t Hk,
+                                 int32_t dh, uint8_t* __restrict__ dst, int64_t dst_rows, int64_t dst_row0) {
+  const int row_bytes = dh * eb;
+  const int cpr = row_bytes / 16;
+  const int64_t units = static_cast<int64_t>(n_tok) * L * 2 * Hk * cpr;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
+       u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(u % cpr);
+    const int64_t p = u / cpr;  // ((t*L + l)*2 + kv)*Hk + h
+    const int64_t t = p / (static_cast<int64_t>(L) * 2 * Hk);
+    const int64_t plane = p % (static_cast<int64_t>(L) * 2 * Hk);
+    const uint4 v = *reinterpret_cast<const uint4*>(src + p * row_bytes + c * 16);
+    *reinterpret_cast<uint4*>(dst + (plane * dst_rows + dst_row0 + t) * row_bytes + c * 16) = v;
+  }
+}
+
+__global__ void k_scale_transpose(const float* __restrict__ src, int32_t n_tok, int32_t planes, float* __restrict__ dst,
+                                  int64_t dst_rows, int64_t dst_row0) {
+  const int64_t units = static_cast<int64_t>(n_tok) * planes;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
+       u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = u / planes, plane = u % planes;
+    dst[plane * dst_rows + dst_row0 + t] = src[u];
+  }
+}
+
+// rows [src_row0, +n_rows) of every plane of a [planes][src_rows][row_bytes] pool (local or a
+// mapped peer pool: one-sided NVLink reads) -> [planes][dst_rows] at dst_row0
+__global__ void k_copy_rows(const uint8_t* __restrict__ src, int64_t src_rows, int64_t src_row0, uint8_t* __restrict__ dst,
+                            int64_t dst_rows, int64_t dst_row0, int32_t n_rows, int32_t planes, int32_t row_bytes) {
+  const int cpr = row_bytes / 16;
+  const int64_t units = static_cast<int64_t>(planes) * n_rows * cpr;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
+       u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(u % cpr);
+    const int64_t r = (u / cpr) % n_rows;
+    const int64_t plane = u / (static_cast<int64_t>(cpr) * n_rows);
+    const uint4 v = *reinterpret_cast<const uint4*>(src + (plane * src_rows + src_row0 + r) * row_bytes + c * 16);
+    *reinterpret_cast<uint4*>(dst + (plane * dst_rows + dst_row0 + r) * row_bytes + c * 16) = v;
+  }
+}
+
+__global__ void k_read_kv(const uint16_t* __restrict__ arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
+                          int32_t row0, int32_t n, uint16_t* __restrict__ k_out, uint16_t* __restrict__ v_out) {
+  const int64_t units = static_cast<int64_t>(2) * n * Hk * dh;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
+       u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(u % dh);
+    int64_t r = u / dh;
+    const int h = static_cast<int>(r % Hk);
+    r /= Hk;
+    const int t = static_cast<int>(r % n);
+    const int kv = static_cast<int>(r / n);
+    const uint16_t v = arena[(((static_cast<int64_t>(layer) * 2 + kv) * Hk + h) * arena_rows + row0 + t) * dh + j];
+    (kv == 0 ? k_out : v_out)[(static_cast<int64_t>(t) * Hk + h) * dh + j] = v;
+  }
+}
+
+// diagnostic K5: D[i] = sum_j term(k_new, k_st) + term(v_new, v_st) over `width` elements, one warp per row
+__global__ void k_dev_diag(const uint16_t* kn, const uint16_t* ks, const uint16_t* vn, const uint16_t* vs, int32_t n,
+                           int32_t width, unsigned long long* out) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  unsigned long long acc = 0;
+  const int64_t b = static_cast<int64_t>(row) * width;
+  for (int j = lane; j < width; j += 32) {
+    acc += dev_term(bf2f(kn[b + j]), ks[b + j]);
+    acc += dev_term(bf2f(vn[b + j]), vs[b + j]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+  if (lane == 0) out[row] = acc;
+}
+
+inline int blocks_for(int64_t units, int per = 256, int cap = 148 * 16) {
+  int64_t b = (units + per - 1) / per;
+  if (b < 1) b = 1;
+  return static_cast<int>(b > cap ? cap : b);
+}
+}  // namespace
+
+cudaError_t embed_launch(const uint16_t* emb, const int32_t* tok, int32_t rows, int32_t d, float* x, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  k_embed<<<blocks_for(static_cast<int64_t>(rows) * d / 8), 256, 0, s>>>(emb, tok, rows, d, x);
+  return cudaGetLastError();
+}
+cudaError_t rmsnorm_launch(const float* x, const int32_t* row_idx, int32_t rows, int32_t d, const uint16_t* g, float eps,
+                           uint16_t* out, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  const int th = d >= 1024 ? 256 : 64;
+  k_rmsnorm<<<rows, th, 0, s>>>(x, row_idx, d, g, eps, out);
+  return cudaGetLastError();
+}
+cudaError_t gather_rows_f32_launch(const float* src, const int32_t* idx, int32_t rows, int32_t d, float* dst,
+                                   cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  k_gather_rows<<<blocks_for(static_cast<int64_t>(rows) * d / 4), 256, 0, s>>>(src, idx, rows, d, dst);
+  return cudaGetLastError();
+}
+cudaError_t select_launch(const SelectArgs& a, cudaStream_t s) {
+  if (a.n_req <= 0) return cudaSuccess;
+  k_select<<<a.n_req, SEL_THREADS, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t dev_diag_launch(const uint16_t* kn, const uint16_t* ks, const uint16_t* vn, const uint16_t* vs, int32_t n,
+                            int32_t width, unsigned long long* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_dev_diag<<<(n + 7) / 8, 256, 0, s>>>(kn, ks, vn, vs, n, width, out);
+  return cudaGetLastError();
+}
+cudaError_t cand_scores_launch(const float* logits, int64_t vocab, const int32_t* cand_req, const int32_t* idtok,
+                               int32_t n, float* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_cand_scores<<<(n + 255) / 256, 256, 0, s>>>(logits, vocab, cand_req, idtok, n, out);
+  return cudaGetLastError();
+}
+cudaError_t pool_transpose_launch(const void* src, int eb, int32_t n_tok, int32_t L, int32_t Hk, int32_t dh, void* dst,
+                                  int64_t dst_rows, int64_t dst_row0, cudaStream_t s) {
+  if (n_tok <= 0) return cudaSuccess;
+  if ((dh * eb) % 16) return cudaErrorInvalidValue;
+  const int64_t units = static_cast<int64_t>(n_tok) * L * 2 * Hk * (dh * eb / 16);
+  k_pool_transpose<<<blocks_for(units), 256, 0, s>>>(static_cast<const uint8_t*>(src), eb, n_tok, L, Hk, dh,
+                                                     static_cast<uint8_t*>(dst), dst_rows, dst_row0);
+  return cudaGetLastError();
+}
+cudaError_t scale_transpose_launch(const float* src, int32_t n_tok, int32_t L, int32_t Hk, float* dst, int64_t dst_rows,
+                                   int64_t dst_row0, cudaStream_t s) {
+  if (n_tok <= 0) return cudaSuccess;
+  k_scale_transpose<<<blocks_for(static_cast<int64_t>(n_tok) * L * 2 * Hk), 256, 0, s>>>(src, n_tok, L * 2 * Hk, dst,
+                                                                                         dst_rows, dst_row0);
+  return cudaGetLastError();
+}
+cudaError_t copy_rows_launch(const void* src_base, int64_t src_rows, int64_t src_row0, void* dst_base, int64_t dst_rows,
+                             int64_t dst_row0, int32_t n_rows, int32_t n_planes, int32_t row_bytes, cudaStream_t s) {
+  if (n_rows <= 0) return cudaSuccess;
+  if (row_bytes % 16) return cudaErrorInvalidValue;
+  const int64_t units = static_cast<int64_t>(n_planes) * n_rows * (row_bytes / 16);
+  k_copy_rows<<<blocks_for(units), 256, 0, s>>>(static_cast<const uint8_t*>(src_base), src_rows, src_row0,
+                                                static_cast<uint8_t*>(dst_base), dst_rows, dst_row0, n_rows, n_planes,
+                                                row_bytes);
+  return cudaGetLastError();
+}
+cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh, int32_t row0,
+                           int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_read_kv<<<blocks_for(static_cast<int64_t>(2) * n * Hk * dh), 256, 0, s>>>(arena, arena_rows, layer, Hk, dh, row0, n,
+                                                                             k_out, v_out);
+  return cudaGetLastError();
+}
+
+}  // namespace rc

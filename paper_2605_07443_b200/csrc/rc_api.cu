@@ -1,0 +1,1124 @@
+// librc host side: the C-ABI of include/rc.h -- context, pools, request assembly (a0/a1) and
+// the selective-prefill layer loop (a2-a8). All arithmetic of the path runs in the kernels of
+// k_gather.cu, k_gemm.cu, k_attn.cu and k_small.cu; this file does allocation, metadata and
+// launch order only.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/rc.h"
+#include "rc_internal.h"
+
+using namespace rc;
+
+namespace {
+
+thread_local std::string g_err;
+
+rc_status fail(rc_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define RC_CUDA(expr)                                                                        \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(RC_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// First-fit range allocator over [0, cap) with coalescing free list.
+struct RangeAlloc {
+  int64_t cap = 0;
+  std::map<int64_t, int64_t> free_;  // start -> len
+  void init(int64_t c) {
+    cap = c;
+    free_.clear();
+    if (c > 0) free_[0] = c;
+  }
+  int64_t alloc(int64_t len) {
+    if (len <= 0) return 0;
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second >= len) {
+        const int64_t s = it->first, l = it->second;
+        free_.erase(it);
+        if (l > len) free_[s + len] = l - len;
+        return s;
+      }
+    }
+    return -1;
+  }
+  void release(int64_t s, int64_t len) {
+    if (len <= 0) return;
+    auto it = free_.emplace(s, len).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+};
+
+struct Block {
+  int64_t row;
+  int32_t n;
+  int32_t canon;
+  bool remote;
+  uint64_t last_use;
+};
+
+struct Seq {
+  int32_t n = 0, P = 0, gather_from = 0;
+  int64_t arena_row = 0;
+  std::vector<int32_t> tokens;
+  std::vector<uint8_t> cls;  // after miss handling
+  std::vector<int32_t> cand_idtok;
+};
+
+// Pinned host staging with per-slot events so the host never overwrites an in-flight copy.
+struct Staging {
+  static constexpr int SLOTS = 4;
+  void* host[SLOTS] = {};
+  void* dev[SLOTS] = {};
+  size_t cap[SLOTS] = {};
+  cudaEvent_t ev[SLOTS] = {};
+  int next = 0;
+  ~Staging() {
+    for (int i = 0; i < SLOTS; ++i) {
+      if (host[i]) cudaFreeHost(host[i]);
+      if (dev[i]) cudaFree(dev[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+  // returns slot index; host[slot] has >= bytes
+  int acquire(size_t bytes, cudaError_t* err) {
+    const int s = next;
+    next = (next + 1) % SLOTS;
+    *err = cudaSuccess;
+    if (ev[s]) {
+      *err = cudaEventSynchronize(ev[s]);
+      if (*err != cudaSuccess) return -1;
+    } else {
+      *err = cudaEventCreateWithFlags(&ev[s], cudaEventDisableTiming);
+      if (*err != cudaSuccess) return -1;
+    }
+    if (cap[s] < bytes) {
+      if (host[s]) cudaFreeHost(host[s]);
+      if (dev[s]) cudaFree(dev[s]);
+      host[s] = dev[s] = nullptr;
+      const size_t c = std::max(bytes, static_cast<size_t>(1) << 20);
+      *err = cudaMallocHost(&host[s], c);
+      if (*err == cudaSuccess) *err = cudaMalloc(&dev[s], c);
+      if (*err != cudaSuccess) { cap[s] = 0; return -1; }
+      cap[s] = c;
+    }
+    return s;
+  }
+};
+
+// Bump layout of several arrays inside one staging slot (16-byte aligned pieces).
+struct Layout {
+  size_t off = 0;
+  size_t add(size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return o;
+  }
+};
+
+template <typename T>
+T* dev_alloc(size_t n, cudaError_t* e) {
+  void* p = nullptr;
+  *e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct rc_ctx {
+  int device = 0;
+  int num_sms = 148;
+  rc_model_desc m{};
+  rc_pool_desc pd{};
+  // weights
+  const uint16_t* embed = nullptr;
+  const uint16_t* fnorm = nullptr;
+  const uint16_t* lm_head = nullptr;
+  std::vector<const uint16_t*> ln1, ln2, wo, wd;
+  uint16_t* wqkv = nullptr;  // [L][Nqkv][d]
+  uint16_t* bqkv = nullptr;  // [L][Nqkv]
+  uint16_t* wgu = nullptr;   // [L][2F][d]
+  int Nqkv = 0;
+  // pools ([L][2][Hk][rows][dh])
+  uint16_t* item_pool = nullptr;
+  int8_t* hist_q = nullptr;
+  float* hist_s = nullptr;
+  uint16_t* prefix_pool = nullptr;
+  RangeAlloc item_alloc, remote_alloc;
+  int64_t hist_used = 0, prefix_used = 0;
+  std::unordered_map<uint64_t, Block> items, protos, prefixes;
+  uint64_t use_clock = 1;
+  // peers
+  std::unordered_map<int, std::pair<const uint16_t*, int64_t>> peers;  // rank -> (pool base, rows)
+  std::vector<void*> ipc_opened;
+  // arena
+  uint16_t* arena = nullptr;
+  RangeAlloc arena_alloc;
+  std::unordered_map<uint64_t, Seq> seqs;
+  uint64_t next_seq = 1;
+  // rope tables
+  float* rope_cos = nullptr;
+  float* rope_sin = nullptr;
+  int32_t rope_zero = 0;
+  // workspace
+  int64_t Mx = 0;
+  float* x = nullptr;
+  float* xs = nullptr;
+  uint16_t* a = nullptr;
+  uint16_t* q = nullptr;
+  uint16_t* o = nullptr;
+  uint16_t* h = nullptr;
+  unsigned long long* dev = nullptr;
+  float* logits = nullptr;
+  int64_t logits_rows = 0;
+  int32_t* sel_pos = nullptr;
+  int32_t* sel_dst = nullptr;
+  int32_t* sel_urow = nullptr;
+  // tensor maps
+  CUtensorMap mA_a{}, mA_o{}, mA_h{};
+  std::vector<CUtensorMap> mB_qkv, mB_kv, mB_o, mB_gu, mB_d;
+  CUtensorMap mB_lm{};
+  int bn_qkv = 256, bn_kv = 256, bn_o = 256, bn_d = 256, bn_lm = 256;
+  Staging stage;
+  int64_t launches = 0;
+  // profiling (rc_profile_begin / rc_profile_end): CUDA events around every librc launch
+  struct Rec { int kind; cudaEvent_t a, b; double flops, bytes; int pending; };
+  struct Pending { int32_t* host; int32_t S; std::vector<std::pair<int, int>> ranges; int layers; };
+  bool prof = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> evpool;
+  size_t ev_used = 0;
+  std::vector<Pending> pend;
+
+  ~rc_ctx() {
+    cudaSetDevice(device);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    for (auto& p : pend) cudaFreeHost(p.host);
+    void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
+                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow};
+    for (void* p : bufs)
+      if (p) cudaFree(p);
+  }
+};
+
+namespace {
+int pick_bn(int N) { return N > 128 ? 256 : 128; }
+
+cudaEvent_t next_ev(rc_ctx* c) {
+  if (c->ev_used == c->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->ev_used++];
+}
+// Every librc kernel launch goes through RC_LAUNCH: counted, and timed per kind when profiling.
+#define RC_LAUNCH(kind, flops, bytes, pending, expr)                                                     \
+  do {                                                                                                  \
+    c->launches++;                                                                                      \
+    cudaEvent_t a_ = nullptr, b_ = nullptr;                                                             \
+    if (c->prof) { a_ = next_ev(c); b_ = next_ev(c); cudaEventRecord(a_, s); }                          \
+    cudaError_t e_ = (expr);                                                                            \
+    if (e_ != cudaSuccess) return fail(RC_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    if (c->prof) {                                                                                      \
+      cudaEventRecord(b_, s);                                                                           \
+      c->recs.push_back({kind, a_, b_, static_cast<double>(flops), static_cast<double>(bytes), pending}); \
+    }                                                                                                   \
+  } while (0)
+double gemm_flops(double M, double N, double K) { return 2.0 * M * N * K; }
+double gemm_bytes(double M, double N, double K, double out_b) { return (M * K + N * K) * 2.0 + M * N * out_b; }
+
+rc_status build_rope(rc_ctx* c) {
+  const int dh = c->m.head_dim, half = dh / 2;
+  const int zero = c->pd.max_seq_len;
+  const int64_t rows = 2 * static_cast<int64_t>(zero) + 1;
+  std::vector<double> inv(half);
+  for (int i = 0; i < half; ++i) inv[i] = std::pow(c->m.rope_theta, (-2.0 * i) / dh);
+  std::vector<float> cs(rows * half), sn(rows * half);
+  for (int64_t r = 0; r < rows; ++r) {
+    const double d = static_cast<double>(r - zero);
+    for (int i = 0; i < half; ++i) {
+      const double ang = d * inv[i];
+      cs[r * half + i] = static_cast<float>(std::cos(ang));
+      sn[r * half + i] = static_cast<float>(std::sin(ang));
+    }
+  }
+  cudaError_t e;
+  c->rope_cos = dev_alloc<float>(rows * half, &e);
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "rope table alloc");
+  c->rope_sin = dev_alloc<float>(rows * half, &e);
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "rope table alloc");
+  RC_CUDA(cudaMemcpy(c->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(c->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  c->rope_zero = zero;
+  return RC_OK;
+}
+
+int64_t plane_count(const rc_ctx* c) { return static_cast<int64_t>(c->m.n_layers) * 2 * c->m.n_kv_heads; }
+
+uint16_t* arena_layer(rc_ctx* c, int l, int kv) {
+  return c->arena + (static_cast<int64_t>(l) * 2 + kv) * c->m.n_kv_heads * c->pd.arena_rows * c->m.head_dim;
+}
+}  // namespace
+
+extern "C" {
+
+const char* rc_last_error(void) { return g_err.c_str(); }
+int32_t rc_abi_version(void) { return 1; }
+int64_t rc_launch_count(rc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_desc* pd, int32_t device, rc_ctx** out) {
+  if (!md || !w || !pd || !out) return fail(RC_E_INVALID, "null argument");
+  const rc_model_desc& m = *md;
+  if (m.n_layers <= 0 || m.d_model <= 0 || m.n_heads <= 0 || m.n_kv_heads <= 0 || m.n_heads % m.n_kv_heads ||
+      !(m.head_dim == 16 || m.head_dim == 64 || m.head_dim == 128) || m.d_ff % 128 || m.d_model % 64 != 0 &&
+      m.d_model % 16 != 0)
+    return fail(RC_E_INVALID, "unsupported model shape");
+  if (pd->max_seq_len <= 0 || pd->max_seq_len > 8192) return fail(RC_E_INVALID, "max_seq_len must be in 1..8192 (R6)");
+  if (pd->max_batch_tokens <= 0 || pd->remote_rows > pd->item_rows) return fail(RC_E_INVALID, "bad pool desc");
+  if (!w->embed || !w->final_norm || !w->lm_head || !w->ln1 || !w->wq || !w->wk || !w->wv || !w->wo || !w->ln2 ||
+      !w->wg || !w->wu || !w->wd || (m.qkv_bias && (!w->bq || !w->bk || !w->bv)))
+    return fail(RC_E_INVALID, "missing weight pointer");
+  std::unique_ptr<rc_ctx> c(new rc_ctx());
+  c->device = device;
+  c->m = m;
+  c->pd = *pd;
+  RC_CUDA(cudaSetDevice(device));
+  RC_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  const int L = m.n_layers, d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
+  c->Nqkv = (H + 2 * Hk) * dh;
+  c->embed = static_cast<const uint16_t*>(w->embed);
+  c->fnorm = static_cast<const uint16_t*>(w->final_norm);
+  c->lm_head = static_cast<const uint16_t*>(w->lm_head);
+  cudaError_t e;
+  c->wqkv = dev_alloc<uint16_t>(static_cast<size_t>(L) * c->Nqkv * d, &e);
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "packed qkv weights");
+  c->wgu = dev_alloc<uint16_t>(static_cast<size_t>(L) * 2 * F * d, &e);
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "packed gate/up weights");
+  if (m.qkv_bias) {
+    c->bqkv = dev_alloc<uint16_t>(static_cast<size_t>(L) * c->Nqkv, &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "packed qkv bias");
+  }
+  for (int l = 0; l < L; ++l) {
+    c->ln1.push_back(static_cast<const uint16_t*>(w->ln1[l]));
+    c->ln2.push_back(static_cast<const uint16_t*>(w->ln2[l]));
+    c->wo.push_back(static_cast<const uint16_t*>(w->wo[l]));
+    c->wd.push_back(static_cast<const uint16_t*>(w->wd[l]));
+    uint16_t* dq = c->wqkv + static_cast<size_t>(l) * c->Nqkv * d;
+    RC_CUDA(cudaMemcpy(dq, w->wq[l], static_cast<size_t>(H) * dh * d * 2, cudaMemcpyDeviceToDevice));
+    RC_CUDA(cudaMemcpy(dq + static_cast<size_t>(H) * dh * d, w->wk[l], static_cast<size_t>(Hk) * dh * d * 2,
+                       cudaMemcpyDeviceToDevice));
+    RC_CUDA(cudaMemcpy(dq + static_cast<size_t>(H + Hk) * dh * d, w->wv[l], static_cast<size_t>(Hk) * dh * d * 2,
+                       cudaMemcpyDeviceToDevice));
+    if (m.qkv_bias) {
+      uint16_t* db = c->bqkv + static_cast<size_t>(l) * c->Nqkv;
+      RC_CUDA(cudaMemcpy(db, w->bq[l], static_cast<size_t>(H) * dh * 2, cudaMemcpyDeviceToDevice));
+      RC_CUDA(cudaMemcpy(db + H * dh, w->bk[l], static_cast<size_t>(Hk) * dh * 2, cudaMemcpyDeviceToDevice));
+      RC_CUDA(cudaMemcpy(db + (H + Hk) * dh, w->bv[l], static_cast<size_t>(Hk) * dh * 2, cudaMemcpyDeviceToDevice));
+    }
+    // gate/up interleaved in 128-row chunks: [g 0..127 | u 0..127 | g 128..255 | u 128..255 | ...]
+    uint16_t* dg = c->wgu + static_cast<size_t>(l) * 2 * F * d;
+    const size_t chunk = static_cast<size_t>(128) * d * 2;
+    RC_CUDA(cudaMemcpy2D(dg, 2 * chunk, w->wg[l], chunk, chunk, F / 128, cudaMemcpyDeviceToDevice));
+    RC_CUDA(cudaMemcpy2D(reinterpret_cast<uint8_t*>(dg) + chunk, 2 * chunk, w->wu[l], chunk, chunk, F / 128,
+                         cudaMemcpyDeviceToDevice));
+  }
+  // pools + arena
+  const int64_t planes = static_cast<int64_t>(L) * 2 * Hk;
+  if (pd->item_rows > 0) {
+    c->item_pool = dev_alloc<uint16_t>(static_cast<size_t>(planes) * pd->item_rows * dh, &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "item pool");
+  }
+  c->item_alloc.init(pd->item_rows - pd->remote_rows);
+  c->remote_alloc.init(pd->remote_rows);
+  if (pd->hist_rows > 0) {
+    c->hist_q = dev_alloc<int8_t>(static_cast<size_t>(planes) * pd->hist_rows * dh, &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "history pool");
+    c->hist_s = dev_alloc<float>(static_cast<size_t>(planes) * pd->hist_rows, &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "history scales");
+  }
+  if (pd->prefix_rows > 0) {
+    c->prefix_pool = dev_alloc<uint16_t>(static_cast<size_t>(planes) * pd->prefix_rows * dh, &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "prefix pool");
+  }
+  c->arena = dev_alloc<uint16_t>(static_cast<size_t>(planes) * std::max<int64_t>(pd->arena_rows, 1) * dh, &e);
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "stitched-KV arena");
+  c->arena_alloc.init(pd->arena_rows);
+  rc_status st = build_rope(c.get());
+  if (st != RC_OK) return st;
+  // workspace
+  const int64_t Mx = pd->max_batch_tokens;
+  c->Mx = Mx;
+  c->x = dev_alloc<float>(Mx * d, &e); if (e) return fail(RC_E_NOMEM, "workspace x");
+  c->xs = dev_alloc<float>(Mx * d, &e); if (e) return fail(RC_E_NOMEM, "workspace xs");
+  c->a = dev_alloc<uint16_t>(Mx * d, &e); if (e) return fail(RC_E_NOMEM, "workspace a");
+  c->q = dev_alloc<uint16_t>(Mx * H * dh, &e); if (e) return fail(RC_E_NOMEM, "workspace q");
+  c->o = dev_alloc<uint16_t>(Mx * H * dh, &e); if (e) return fail(RC_E_NOMEM, "workspace o");
+  c->h = dev_alloc<uint16_t>(Mx * F, &e); if (e) return fail(RC_E_NOMEM, "workspace h");
+  c->dev = dev_alloc<unsigned long long>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace dev");
+  c->sel_pos = dev_alloc<int32_t>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace sel");
+  c->sel_dst = dev_alloc<int32_t>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace sel");
+  c->sel_urow = dev_alloc<int32_t>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace sel");
+  // tensor maps: A operands (rows = Mx; tiles never read beyond the call's M-tile), B = weights
+  bool ok = make_tmap_bf16_2d(&c->mA_a, c->a, Mx, d, d, 128) &&
+            make_tmap_bf16_2d(&c->mA_o, c->o, Mx, H * dh, H * dh, 128) &&
+            make_tmap_bf16_2d(&c->mA_h, c->h, Mx, F, F, 128);
+  c->bn_qkv = pick_bn(c->Nqkv);
+  c->bn_kv = pick_bn(2 * Hk * dh);
+  c->bn_o = pick_bn(d);
+  c->bn_d = pick_bn(d);
+  c->bn_lm = 256;
+  c->mB_qkv.resize(L); c->mB_kv.resize(L); c->mB_o.resize(L); c->mB_gu.resize(L); c->mB_d.resize(L);
+  for (int l = 0; l < L && ok; ++l) {
+    const uint16_t* wq = c->wqkv + static_cast<size_t>(l) * c->Nqkv * d;
+    ok = ok && make_tmap_bf16_2d(&c->mB_qkv[l], wq, c->Nqkv, d, d, c->bn_qkv);
+    ok = ok && make_tmap_bf16_2d(&c->mB_kv[l], wq + static_cast<size_t>(H) * dh * d, 2 * Hk * dh, d, d, c->bn_kv);
+    ok = ok && make_tmap_bf16_2d(&c->mB_o[l], c->wo[l], d, H * dh, H * dh, c->bn_o);
+    ok = ok && make_tmap_bf16_2d(&c->mB_gu[l], c->wgu + static_cast<size_t>(l) * 2 * F * d, 2 * F, d, d, 256);
+    ok = ok && make_tmap_bf16_2d(&c->mB_d[l], c->wd[l], d, F, F, c->bn_d);
+  }
+  ok = ok && make_tmap_bf16_2d(&c->mB_lm, c->lm_head, m.vocab, d, d, c->bn_lm);
+  if (!ok) return fail(RC_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or alignment)");
+  RC_CUDA(cudaDeviceSynchronize());
+  *out = c.release();
+  return RC_OK;
+}
+
+void rc_destroy(rc_ctx* ctx) { delete ctx; }
+
+rc_status rc_decompose_prompt(const rc_prompt* pr, int32_t cap, int32_t* n_out, int32_t* token_ids, uint8_t* cls,
+                              int64_t* src_id, int32_t* src_off, int32_t* seg_start) {
+  if (!pr || !n_out) return fail(RC_E_INVALID, "null argument");
+  if (pr->prefix_len < 0 || pr->n_hist < 0 || pr->n_cand < 0 || pr->n_tail < 0)
+    return fail(RC_E_INVALID, "negative segment length");
+  int64_t n = static_cast<int64_t>(pr->prefix_len) + pr->n_hist + pr->n_tail;
+  for (int i = 0; i < pr->n_cand; ++i) {
+    if (pr->cand_len[i] <= 0) return fail(RC_E_INVALID, "empty candidate block");
+    n += pr->cand_len[i];
+  }
+  if (n > cap) return fail(RC_E_CAPACITY, "prompt longer than output capacity");
+  int32_t p = 0, seg = 0;
+  auto put = [&](int32_t t, uint8_t c, int64_t id, int32_t off) {
+    token_ids[p] = t; cls[p] = c; src_id[p] = id; src_off[p] = off; ++p;
+  };
+  if (seg_start) seg_start[seg++] = p;
+  for (int i = 0; i < pr->prefix_len; ++i) put(pr->prefix_tokens[i], RC_TOK_PREFIX, -1, 0);
+  if (seg_start) seg_start[seg++] = p;
+  for (int i = 0; i < pr->n_hist; ++i) put(pr->hist_tokens[i], RC_TOK_HIST, pr->hist_proto[i], 0);
+  int64_t ct = 0;
+  for (int c = 0; c < pr->n_cand; ++c) {
+    if (seg_start) seg_start[seg++] = p;
+    for (int j = 0; j < pr->cand_len[c]; ++j) put(pr->cand_tokens[ct + j], RC_TOK_ITEM, pr->cand_item[c], j);
+    ct += pr->cand_len[c];
+  }
+  if (seg_start) seg_start[seg++] = p;
+  for (int i = 0; i < pr->n_tail; ++i) put(pr->tail_tokens[i], RC_TOK_FORCED, -1, 0);
+  *n_out = p;
+  return RC_OK;
+}
+
+rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, const uint64_t* ids, const int32_t* n_tokens,
+                                  const int32_t* canon_pos, const void* kv, const float* scales, rc_stream stream) {
+  if (!c || n_blocks < 0 || (n_blocks > 0 && (!ids || !n_tokens || !canon_pos || !kv)))
+    return fail(RC_E_INVALID, "null argument");
+  if (n_blocks == 0) return RC_OK;
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto* dir = kind == RC_POOL_ITEM_BF16 ? &c->items : kind == RC_POOL_HIST_INT8 ? &c->protos
+              : kind == RC_POOL_PREFIX_BF16 ? &c->prefixes : nullptr;
+  if (!dir) return fail(RC_E_INVALID, "unknown pool kind");
+  if (kind == RC_POOL_HIST_INT8 && !scales) return fail(RC_E_INVALID, "history blocks need scales");
+  int64_t total = 0;
+  for (int i = 0; i < n_blocks; ++i) {
+    if (n_tokens[i] <= 0) return fail(RC_E_INVALID, "empty block");
+    if (kind == RC_POOL_HIST_INT8 && n_tokens[i] != 1) return fail(RC_E_INVALID, "prototype blocks are single tokens");
+    if (kind == RC_POOL_PREFIX_BF16 && canon_pos[i] != 0) return fail(RC_E_INVALID, "prefix blocks start at 0");
+    if (dir->count(ids[i])) return fail(RC_E_EXISTS, "duplicate block id " + std::to_string(ids[i]));
+    for (int j = 0; j < i; ++j)
+      if (ids[j] == ids[i]) return fail(RC_E_EXISTS, "duplicate block id in call");
+    total += n_tokens[i];
+  }
+  int64_t row0;
+  int64_t rows_cap;
+  if (kind == RC_POOL_ITEM_BF16) {
+    row0 = c->item_alloc.alloc(total);
+    if (row0 < 0) return fail(RC_E_CAPACITY, "item pool full");
+    rows_cap = c->pd.item_rows;
+  } else if (kind == RC_POOL_HIST_INT8) {
+    if (c->hist_used + total > c->pd.hist_rows) return fail(RC_E_CAPACITY, "history pool full");
+    row0 = c->hist_used;
+    rows_cap = c->pd.hist_rows;
+  } else {
+    if (c->prefix_used + total > c->pd.prefix_rows) return fail(RC_E_CAPACITY, "prefix pool full");
+    row0 = c->prefix_used;
+    rows_cap = c->pd.prefix_rows;
+  }
+  const int L = c->m.n_layers, Hk = c->m.n_kv_heads, dh = c->m.head_dim;
+  cudaError_t e;
+  if (kind == RC_POOL_HIST_INT8) {
+    e = pool_transpose_launch(kv, 1, static_cast<int32_t>(total), L, Hk, dh, c->hist_q, rows_cap, row0, s);
+    if (e == cudaSuccess) e = scale_transpose_launch(scales, static_cast<int32_t>(total), L, Hk, c->hist_s, rows_cap, row0, s);
+    c->launches += 2;  // offline registration: counted, never profiled
+  } else {
+    e = pool_transpose_launch(kv, 2, static_cast<int32_t>(total), L, Hk, dh,
+                              kind == RC_POOL_ITEM_BF16 ? c->item_pool : c->prefix_pool, rows_cap, row0, s);
+    c->launches += 1;
+  }
+  if (e != cudaSuccess) {
+    if (kind == RC_POOL_ITEM_BF16) c->item_alloc.release(row0, total);
+    return fail(RC_E_CUDA, std::string("register copy: ") + cudaGetErrorString(e));
+  }
+  int64_t r = row0;
+  for (int i = 0; i < n_blocks; ++i) {
+    (*dir)[ids[i]] = Block{r, n_tokens[i], canon_pos[i], false, 0};
+    r += n_tokens[i];
+  }
+  if (kind == RC_POOL_HIST_INT8) c->hist_used += total;
+  if (kind == RC_POOL_PREFIX_BF16) c->prefix_used += total;
+  return RC_OK;
+}
+
+rc_status rc_pool_contains(rc_ctx* c, int32_t kind, int32_t n, const uint64_t* ids, uint8_t* out) {
+  if (!c || (n > 0 && (!ids || !out))) return fail(RC_E_INVALID, "null argument");
+  auto* dir = kind == RC_POOL_ITEM_BF16 ? &c->items : kind == RC_POOL_HIST_INT8 ? &c->protos
+              : kind == RC_POOL_PREFIX_BF16 ? &c->prefixes : nullptr;
+  if (!dir) return fail(RC_E_INVALID, "unknown pool kind");
+  for (int i = 0; i < n; ++i) out[i] = dir->count(ids[i]) ? 1 : 0;
+  return RC_OK;
+}
+
+rc_status rc_pool_locate(rc_ctx* c, int32_t n, const uint64_t* ids, int64_t* rows_out) {
+  if (!c || (n > 0 && (!ids || !rows_out))) return fail(RC_E_INVALID, "null argument");
+  for (int i = 0; i < n; ++i) {
+    auto it = c->items.find(ids[i]);
+    rows_out[i] = it == c->items.end() ? -1 : it->second.row;
+  }
+  return RC_OK;
+}
+
+rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t miss_policy, int32_t gather_from,
+                      rc_seq* out_seqs, uint64_t* out_missing, int32_t* n_missing, rc_stream stream) {
+  if (!c || n_req < 0 || (n_req > 0 && (!reqs || !out_seqs))) return fail(RC_E_INVALID, "null argument");
+  if (gather_from < 0 || gather_from > c->m.n_layers) return fail(RC_E_INVALID, "gather_from out of range");
+  if (miss_policy != RC_MISS_ERROR && miss_policy != RC_MISS_RECOMPUTE) return fail(RC_E_INVALID, "miss policy");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // ---- validate + resolve everything before touching state (all-or-nothing)
+  std::vector<Seq> built(n_req);
+  std::vector<uint64_t> missing;
+  std::vector<int4> meta_all, meta_pre;  // {dst_row(rel), src_row, delta, kind}; dst fixed up after alloc
+  std::vector<int> meta_all_req, meta_pre_req;
+  for (int r = 0; r < n_req; ++r) {
+    const rc_request& q = reqs[r];
+    if (q.n <= 0 || q.n > c->pd.max_seq_len) return fail(RC_E_INVALID, "request length out of range");
+    if (!q.token_ids || !q.cls || !q.src_id || !q.src_off || (q.n_cand > 0 && !q.cand_idtok))
+      return fail(RC_E_INVALID, "null request array");
+    Seq& sq = built[r];
+    sq.n = q.n;
+    sq.gather_from = gather_from;
+    sq.tokens.assign(q.token_ids, q.token_ids + q.n);
+    sq.cls.assign(q.cls, q.cls + q.n);
+    sq.cand_idtok.assign(q.cand_idtok, q.cand_idtok + q.n_cand);
+    int P = 0;
+    while (P < q.n && q.cls[P] == RC_TOK_PREFIX) ++P;
+    sq.P = P;
+    const Block* pre = nullptr;
+    if (P > 0) {
+      auto it = c->prefixes.find(q.prefix_id);
+      if (it == c->prefixes.end()) return fail(RC_E_NOTFOUND, "prefix block not registered");
+      if (it->second.n < P) return fail(RC_E_INVALID, "prefix block shorter than the request's prefix");
+      pre = &it->second;
+    }
+    for (int p = 0; p < q.n; ++p) {
+      const int k = q.cls[p];
+      if (q.token_ids[p] < 0 || q.token_ids[p] >= c->m.vocab) return fail(RC_E_INVALID, "token id out of range");
+      if (k > RC_TOK_ITEM) return fail(RC_E_INVALID, "bad token class");
+      if (k == RC_TOK_PREFIX) {
+        if (p >= P) return fail(RC_E_INVALID, "PREFIX tokens must be the leading positions");
+        meta_all.push_back(make_int4(p, static_cast<int>(pre->row + p), 0, RC_TOK_PREFIX));
+        meta_all_req.push_back(r);
+        if (gather_from > 0) { meta_pre.push_back(meta_all.back()); meta_pre_req.push_back(r); }
+      } else if (k == RC_TOK_HIST) {
+        auto it = c->protos.find(static_cast<uint64_t>(q.src_id[p]));
+        if (it == c->protos.end()) return fail(RC_E_NOTFOUND, "prototype not registered: " + std::to_string(q.src_id[p]));
+        meta_all.push_back(make_int4(p, static_cast<int>(it->second.row), p - it->second.canon, RC_TOK_HIST));
+        meta_all_req.push_back(r);
+      } else if (k == RC_TOK_ITEM) {
+        auto it = c->items.find(static_cast<uint64_t>(q.src_id[p]));
+        if (it == c->items.end() || q.src_off[p] < 0 || q.src_off[p] >= it->second.n) {
+          if (it == c->items.end()) {
+            if (std::find(missing.begin(), missing.end(), static_cast<uint64_t>(q.src_id[p])) == missing.end())
+              missing.push_back(static_cast<uint64_t>(q.src_id[p]));
+            sq.cls[p] = RC_TOK_FORCED;
+            continue;
+          }
+          return fail(RC_E_INVALID, "item offset outside its block");
+        }
+        it->second.last_use = c->use_clock;
+        const int delta = p - (it->second.canon + q.src_off[p]);
+        meta_all.push_back(make_int4(p, static_cast<int>(it->second.row + q.src_off[p]), delta, RC_TOK_ITEM));
+        meta_all_req.push_back(r);
+      }
+    }
+  }
+  ++c->use_clock;
+  if (!missing.empty() && miss_policy == RC_MISS_ERROR) {
+    if (n_missing) {
+      const int cap = *n_missing;
+      for (int i = 0; i < static_cast<int>(missing.size()) && i < cap && out_missing; ++i) out_missing[i] = missing[i];
+      *n_missing = static_cast<int32_t>(missing.size());
+    }
+    return fail(RC_E_NOTFOUND, "candidate item blocks not resident");
+  }
+  if (n_missing) {
+    const int cap = *n_missing;
+    for (int i = 0; i < static_cast<int>(missing.size()) && i < cap && out_missing; ++i) out_missing[i] = missing[i];
+    *n_missing = static_cast<int32_t>(missing.size());
+  }
+  // ---- allocate stitched ranges
+  std::vector<int64_t> rows(n_req);
+  for (int r = 0; r < n_req; ++r) {
+    rows[r] = c->arena_alloc.alloc(built[r].n);
+    if (rows[r] < 0) {
+      for (int j = 0; j < r; ++j) c->arena_alloc.release(rows[j], built[j].n);
+      return fail(RC_E_CAPACITY, "stitched-KV arena full");
+    }
+    built[r].arena_row = rows[r];
+  }
+  for (size_t i = 0; i < meta_all.size(); ++i) meta_all[i].x += static_cast<int>(rows[meta_all_req[i]]);
+  for (size_t i = 0; i < meta_pre.size(); ++i) meta_pre[i].x += static_cast<int>(rows[meta_pre_req[i]]);
+  // ---- metadata H2D + gather
+  const size_t bytes = (meta_all.size() + meta_pre.size()) * sizeof(int4);
+  if (bytes > 0) {
+    cudaError_t e;
+    const int slot = c->stage.acquire(bytes, &e);
+    if (slot < 0) {
+      for (int r = 0; r < n_req; ++r) c->arena_alloc.release(rows[r], built[r].n);
+      return fail(RC_E_NOMEM, std::string("staging: ") + cudaGetErrorString(e));
+    }
+    int4* hm = static_cast<int4*>(c->stage.host[slot]);
+    std::copy(meta_all.begin(), meta_all.end(), hm);
+    std::copy(meta_pre.begin(), meta_pre.end(), hm + meta_all.size());
+    int4* dm = static_cast<int4*>(c->stage.dev[slot]);
+    RC_CUDA(cudaMemcpyAsync(dm, hm, bytes, cudaMemcpyHostToDevice, s));
+    RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
+    GatherArgs g{};
+    g.n_kv_heads = c->m.n_kv_heads;
+    g.head_dim = c->m.head_dim;
+    g.item_pool = c->item_pool; g.item_rows = c->pd.item_rows;
+    g.hist_q = c->hist_q; g.hist_s = c->hist_s; g.hist_rows = c->pd.hist_rows;
+    g.prefix_pool = c->prefix_pool; g.prefix_rows = c->pd.prefix_rows;
+    g.arena = c->arena; g.arena_rows = c->pd.arena_rows;
+    g.rope_cos = c->rope_cos; g.rope_sin = c->rope_sin; g.rope_zero = c->rope_zero;
+    // algorithmic bytes of the gather: every stitched element read once from its pool and
+    // written once (bf16 rows 2*dh bytes; int8 rows dh bytes + one fp32 scale)
+    const double row_b = 2.0 * c->m.head_dim, rows_per_tok = 2.0 * c->m.n_kv_heads;
+    double b_all = 0, b_pre = 0;
+    for (auto& t : meta_all) b_all += rows_per_tok * (t.w == RC_TOK_HIST ? (c->m.head_dim + 4.0 + row_b) : 2 * row_b);
+    b_pre = meta_pre.size() * rows_per_tok * 2 * row_b;
+    g.meta = dm; g.n_tok = static_cast<int32_t>(meta_all.size());
+    g.layer_begin = gather_from; g.layer_end = c->m.n_layers;
+    if (g.n_tok > 0 && g.layer_end > g.layer_begin)
+      RC_LAUNCH(RC_K_GATHER, 0, b_all * (g.layer_end - g.layer_begin), -1, gather_launch(g, c->num_sms, s));
+    g.meta = dm + meta_all.size(); g.n_tok = static_cast<int32_t>(meta_pre.size());
+    g.layer_begin = 0; g.layer_end = gather_from;
+    if (g.n_tok > 0 && g.layer_end > g.layer_begin)
+      RC_LAUNCH(RC_K_GATHER, 0, b_pre * (g.layer_end - g.layer_begin), -1, gather_launch(g, c->num_sms, s));
+  }
+  for (int r = 0; r < n_req; ++r) {
+    const uint64_t id = c->next_seq++;
+    c->seqs.emplace(id, std::move(built[r]));
+    out_seqs[r] = id;
+  }
+  return RC_OK;
+}
+
+void rc_release(rc_ctx* c, int32_t n, const rc_seq* seqs) {
+  if (!c || !seqs) return;
+  for (int i = 0; i < n; ++i) {
+    auto it = c->seqs.find(seqs[i]);
+    if (it == c->seqs.end()) continue;
+    c->arena_alloc.release(it->second.arena_row, it->second.n);
+    c->seqs.erase(it);
+  }
+}
+
+namespace {
+struct ReqPlan {
+  const Seq* sq;
+  int32_t u_off, u_cnt, sel_off, sel_cnt, k_h, k_i, forced, window;
+};
+
+int32_t budget(int32_t r_bp, int32_t count) { return static_cast<int32_t>((static_cast<int64_t>(r_bp) * count + 9999) / 10000); }
+
+rc_status plan_requests(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,
+                        std::vector<ReqPlan>& plan) {
+  if (!prm) return fail(RC_E_INVALID, "null params");
+  if (prm->lambda != 1.0f) return fail(RC_E_UNSUPPORTED, "lambda != 1 (attention-mass term, NEXT-1) not built");
+  if (prm->r_rev_bp < 0 || prm->r_rev_bp > 10000 || prm->r_item_bp < 0 || prm->r_item_bp > 10000)
+    return fail(RC_E_INVALID, "recompute ratio out of [0, 10000] bp");
+  if (prm->check_layer < 0 || prm->check_layer >= c->m.n_layers) return fail(RC_E_INVALID, "check_layer out of range");
+  if (prm->window < 0) return fail(RC_E_INVALID, "negative window");
+  plan.resize(n_req);
+  int32_t uo = 0, so = 0;
+  for (int r = 0; r < n_req; ++r) {
+    auto it = c->seqs.find(seqs[r]);
+    if (it == c->seqs.end()) return fail(RC_E_NOTFOUND, "unknown sequence handle");
+    const Seq& sq = it->second;
+    if (prm->check_layer < sq.gather_from)
+      return fail(RC_E_INVALID, "check_layer below the sequence's gather_from (layers not assembled)");
+    ReqPlan& p = plan[r];
+    p.sq = &sq;
+    p.u_off = uo;
+    p.u_cnt = sq.n - sq.P;
+    p.window = prm->window;
+    int nh = 0, ni = 0, nf = 0, nw = 0;
+    for (int pos = sq.P; pos < sq.n; ++pos) {
+      const bool in_win = prm->window > 0 && pos >= sq.n - prm->window;
+      if (in_win) { ++nw; continue; }
+      const int k = sq.cls[pos];
+      nh += k == RC_TOK_HIST; ni += k == RC_TOK_ITEM; nf += k == RC_TOK_FORCED;
+    }
+    p.k_h = budget(prm->r_rev_bp, nh);
+    p.k_i = budget(prm->r_item_bp, ni);
+    p.forced = nf + nw;
+    p.sel_cnt = p.forced + p.k_h + p.k_i;
+    if (p.sel_cnt == 0 || sq.n - 1 < sq.P) return fail(RC_E_INVALID, "request has no recomputed position");
+    p.sel_off = so;
+    uo += p.u_cnt;
+    so += p.sel_cnt;
+  }
+  if (uo > c->Mx) return fail(RC_E_CAPACITY, "batch exceeds max_batch_tokens");
+  return RC_OK;
+}
+}  // namespace
+
+rc_status rc_sel_count(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm, int32_t* counts) {
+  if (!c || !counts) return fail(RC_E_INVALID, "null argument");
+  std::vector<ReqPlan> plan;
+  rc_status st = plan_requests(c, n_req, seqs, prm, plan);
+  if (st != RC_OK) return st;
+  for (int r = 0; r < n_req; ++r) counts[r] = plan[r].sel_cnt;
+  return RC_OK;
+}
+
+namespace {
+// one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
+rc_status run_layer(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_pos, const int32_t* d_dst,
+                    const int4* d_tiles, int32_t n_tiles, double attn_flops, int attn_pending, cudaStream_t s) {
+  const rc_model_desc& m = c->m;
+  const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
+  const double R = rows, norm_b = R * d * 6.0;
+  RC_LAUNCH(RC_K_SMALL, 0, norm_b, -1, rmsnorm_launch(x, nullptr, rows, d, c->ln1[l], m.rms_eps, c->a, s));
+  EpiArgs ep{};
+  ep.bias = c->bqkv ? c->bqkv + static_cast<size_t>(l) * c->Nqkv : nullptr;
+  ep.pos = d_pos; ep.dst_row = d_dst;
+  ep.q_out = c->q; ep.q_ld = H * dh;
+  ep.arena_k = arena_layer(c, l, 0); ep.arena_v = arena_layer(c, l, 1);
+  ep.head_stride = c->pd.arena_rows * dh;
+  ep.rope_cos = c->rope_cos; ep.rope_sin = c->rope_sin; ep.rope_zero = c->rope_zero;
+  ep.n_heads = H; ep.n_kv_heads = Hk; ep.head_dim = dh;
+  RC_LAUNCH(RC_K_GEMM, gemm_flops(R, c->Nqkv, d), gemm_bytes(R, c->Nqkv, d, 2), -1,
+            gemm_launch(&c->mA_a, &c->mB_qkv[l], rows, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s));
+  AttnArgs at{};
+  at.q = c->q; at.o = c->o; at.qpos = d_pos; at.tiles = d_tiles; at.n_tiles = n_tiles;
+  at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
+  at.n_heads = H; at.n_kv_heads = Hk; at.head_dim = dh;
+  at.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
+  RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending, attn_launch(at, s));
+  EpiArgs eo{};
+  eo.out = x; eo.ldo = d;
+  RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, H * dh), gemm_bytes(R, d, H * dh, 8), -1,
+            gemm_launch(&c->mA_o, &c->mB_o[l], rows, d, H * dh, c->bn_o, EPI_ADD_F32, eo, c->num_sms, s));
+  RC_LAUNCH(RC_K_SMALL, 0, norm_b, -1, rmsnorm_launch(x, nullptr, rows, d, c->ln2[l], m.rms_eps, c->a, s));
+  EpiArgs eg{};
+  eg.out = c->h; eg.ldo = F;
+  RC_LAUNCH(RC_K_GEMM, gemm_flops(R, 2.0 * F, d), gemm_bytes(R, 2.0 * F, d, 1), -1,
+            gemm_launch(&c->mA_a, &c->mB_gu[l], rows, 2 * F, d, 256, EPI_SWIGLU, eg, c->num_sms, s));
+  EpiArgs ed{};
+  ed.out = x; ed.ldo = d;
+  RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, F), gemm_bytes(R, d, F, 8), -1,
+            gemm_launch(&c->mA_h, &c->mB_d[l], rows, d, F, c->bn_d, EPI_ADD_F32, ed, c->num_sms, s));
+  return RC_OK;
+}
+}  // namespace
+
+rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm, float* logits,
+                               float* cand_scores, int32_t* sel_pos_out, float* hidden, rc_stream stream) {
+  if (!c || n_req <= 0 || !seqs) return fail(RC_E_INVALID, "null argument / empty batch");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<ReqPlan> plan;
+  rc_status st = plan_requests(c, n_req, seqs, prm, plan);
+  if (st != RC_OK) return st;
+  const rc_model_desc& m = c->m;
+  const int L = m.n_layers, d = m.d_model, cL = prm->check_layer;
+  const int TQ = attn_tokens_per_tile(m.n_heads / m.n_kv_heads);
+  const int32_t U = plan.back().u_off + plan.back().u_cnt;
+  const int32_t S = plan.back().sel_off + plan.back().sel_cnt;
+  int32_t n_cand = 0;
+  for (auto& p : plan) n_cand += static_cast<int32_t>(p.sq->cand_idtok.size());
+  // forced selection (test mode): validate
+  const bool forced = prm->forced_sel != nullptr;
+  if (forced) {
+    if (!prm->forced_sel_off) return fail(RC_E_INVALID, "forced_sel needs forced_sel_off");
+    for (int r = 0; r < n_req; ++r) {
+      const int b = prm->forced_sel_off[r], e = prm->forced_sel_off[r + 1];
+      if (e - b != plan[r].sel_cnt) return fail(RC_E_INVALID, "forced_sel count differs from the budget");
+      const Seq& sq = *plan[r].sq;
+      for (int i = b; i < e; ++i) {
+        const int p = prm->forced_sel[i];
+        if (p < sq.P || p >= sq.n || (i > b && p <= prm->forced_sel[i - 1]))
+          return fail(RC_E_INVALID, "forced_sel positions must be ascending non-prefix positions");
+      }
+      if (prm->forced_sel[e - 1] != sq.n - 1) return fail(RC_E_INVALID, "forced_sel must contain the last position");
+    }
+  }
+  // ---- host tables -> one staging slot
+  Layout lay;
+  const size_t o_tok = lay.add(U * 4), o_pos = lay.add(U * 4), o_dst = lay.add(U * 4), o_cls = lay.add(U),
+               o_reuse = lay.add(U), o_req = lay.add(n_req * 16), o_req2 = lay.add(n_req * 16);
+  int32_t n_ut = 0, n_st = 0;
+  for (auto& p : plan) { n_ut += (p.u_cnt + TQ - 1) / TQ; n_st += (p.sel_cnt + TQ - 1) / TQ; }
+  const size_t o_ut = lay.add(static_cast<size_t>(n_ut) * 16), o_st = lay.add(static_cast<size_t>(n_st) * 16),
+               o_last = lay.add(n_req * 4), o_creq = lay.add(n_cand * 4), o_cid = lay.add(n_cand * 4),
+               o_fsel = lay.add(forced ? static_cast<size_t>(S) * 12 : 0);
+  cudaError_t e;
+  const int slot = c->stage.acquire(lay.off, &e);
+  if (slot < 0) return fail(RC_E_NOMEM, std::string("staging: ") + cudaGetErrorString(e));
+  uint8_t* hb = static_cast<uint8_t*>(c->stage.host[slot]);
+  uint8_t* db = static_cast<uint8_t*>(c->stage.dev[slot]);
+  auto H32 = [&](size_t o) { return reinterpret_cast<int32_t*>(hb + o); };
+  int4* hreq = reinterpret_cast<int4*>(hb + o_req);
+  int4* hreq2 = reinterpret_cast<int4*>(hb + o_req2);
+  int4* hut = reinterpret_cast<int4*>(hb + o_ut);
+  int4* hst = reinterpret_cast<int4*>(hb + o_st);
+  int iu = 0, is = 0, ic = 0;
+  for (int r = 0; r < n_req; ++r) {
+    const ReqPlan& p = plan[r];
+    const Seq& sq = *p.sq;
+    for (int i = 0; i < p.u_cnt; ++i) {
+      const int pos = sq.P + i;
+      H32(o_tok)[p.u_off + i] = sq.tokens[pos];
+      H32(o_pos)[p.u_off + i] = pos;
+      H32(o_dst)[p.u_off + i] = static_cast<int32_t>(sq.arena_row + pos);
+      const bool in_win = p.window > 0 && pos >= sq.n - p.window;
+      hb[o_cls + p.u_off + i] = sq.cls[pos];
+      hb[o_reuse + p.u_off + i] = (!in_win && (sq.cls[pos] == RC_TOK_HIST || sq.cls[pos] == RC_TOK_ITEM)) ? 1 : 0;
+    }
+    hreq[r] = make_int4(p.u_off, p.u_cnt, p.sel_off, sq.n);
+    hreq2[r] = make_int4(p.k_h, p.k_i, static_cast<int>(sq.arena_row), p.window);
+    for (int i = 0; i < p.u_cnt; i += TQ) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), static_cast<int>(sq.arena_row), 0);
+    for (int i = 0; i < p.sel_cnt; i += TQ) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), static_cast<int>(sq.arena_row), 0);
+    H32(o_last)[r] = p.sel_off + p.sel_cnt - 1;
+    for (size_t j = 0; j < sq.cand_idtok.size(); ++j) { H32(o_creq)[ic] = r; H32(o_cid)[ic] = sq.cand_idtok[j]; ++ic; }
+    if (forced) {
+      int32_t* fs = H32(o_fsel);
+      for (int i = 0; i < p.sel_cnt; ++i) {
+        const int pos = prm->forced_sel[prm->forced_sel_off[r] + i];
+        fs[p.sel_off + i] = pos;
+        fs[S + p.sel_off + i] = static_cast<int32_t>(sq.arena_row + pos);
+        fs[2 * S + p.sel_off + i] = p.u_off + (pos - sq.P);
+      }
+    }
+  }
+  RC_CUDA(cudaMemcpyAsync(db, hb, lay.off, cudaMemcpyHostToDevice, s));
+  RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
+  auto D32 = [&](size_t o) { return reinterpret_cast<int32_t*>(db + o); };
+  const int4* d_ut = reinterpret_cast<const int4*>(db + o_ut);
+  const int4* d_st = reinterpret_cast<const int4*>(db + o_st);
+
+  // ---- a2: embedding + full layers l < c over U
+  RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(U) * d * 6.0, -1, embed_launch(c->embed, D32(o_tok), U, d, c->x, s));
+  double attn_u = 0;  // algorithmic attention flops over U: 4 H dh sum_{q in U} (pos_q + 1)
+  for (auto& p : plan)
+    for (int pos = p.sq->P; pos < p.sq->n; ++pos) attn_u += pos + 1.0;
+  attn_u *= 4.0 * m.n_heads * m.head_dim;
+  const int pend_idx = c->prof ? static_cast<int>(c->pend.size()) : -1;
+  for (int l = 0; l < cL; ++l) {
+    st = run_layer(c, l, c->x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, attn_u, -1, s);
+    if (st != RC_OK) return st;
+  }
+  // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
+  if (!forced) {
+    RC_CUDA(cudaMemsetAsync(c->dev, 0, static_cast<size_t>(U) * 8, s));
+    RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(U) * d * 6.0, -1,
+              rmsnorm_launch(c->x, nullptr, U, d, c->ln1[cL], m.rms_eps, c->a, s));
+    EpiArgs ev{};
+    ev.bias = c->bqkv ? c->bqkv + static_cast<size_t>(cL) * c->Nqkv + m.n_heads * m.head_dim : nullptr;
+    ev.pos = D32(o_pos); ev.dst_row = D32(o_dst);
+    ev.arena_k = arena_layer(c, cL, 0); ev.arena_v = arena_layer(c, cL, 1);
+    ev.head_stride = c->pd.arena_rows * m.head_dim;
+    ev.rope_cos = c->rope_cos; ev.rope_sin = c->rope_sin; ev.rope_zero = c->rope_zero;
+    ev.n_heads = m.n_heads; ev.n_kv_heads = m.n_kv_heads; ev.head_dim = m.head_dim;
+    ev.dev_out = c->dev; ev.row_reuse = reinterpret_cast<const uint8_t*>(db + o_reuse);
+    const double Nkv = 2.0 * m.n_kv_heads * m.head_dim;
+    RC_LAUNCH(RC_K_GEMM, gemm_flops(U, Nkv, d), gemm_bytes(U, Nkv, d, 2), -1,
+              gemm_launch(&c->mA_a, &c->mB_kv[cL], U, 2 * m.n_kv_heads * m.head_dim, d, c->bn_kv, EPI_DEV, ev,
+                          c->num_sms, s));
+    // ---- a4: selection
+    SelectArgs sa{};
+    sa.dev = c->dev; sa.ucls = reinterpret_cast<const uint8_t*>(db + o_cls);
+    sa.req = reinterpret_cast<const int4*>(db + o_req); sa.req2 = reinterpret_cast<const int4*>(db + o_req2);
+    sa.n_req = n_req; sa.sel_pos = c->sel_pos; sa.sel_dst = c->sel_dst; sa.sel_urow = c->sel_urow;
+    RC_LAUNCH(RC_K_SELECT, 0, static_cast<double>(U) * 9.0, -1, select_launch(sa, s));
+  } else {
+    const int32_t* fs = D32(o_fsel);
+    RC_CUDA(cudaMemcpyAsync(c->sel_pos, fs, S * 4, cudaMemcpyDeviceToDevice, s));
+    RC_CUDA(cudaMemcpyAsync(c->sel_dst, fs + S, S * 4, cudaMemcpyDeviceToDevice, s));
+    RC_CUDA(cudaMemcpyAsync(c->sel_urow, fs + 2 * S, S * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(S) * d * 8.0, -1,
+            gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
+  // ---- a5-a7: selective layers c..L-1 on Sel
+  for (int l = cL; l < L; ++l) {
+    st = run_layer(c, l, c->xs, S, c->sel_pos, c->sel_dst, d_st, n_st, 0.0, pend_idx, s);
+    if (st != RC_OK) return st;
+  }
+  // ---- a8: final norm on each request's last position, LM head, candidate readout
+  RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(n_req) * d * 6.0, -1,
+            rmsnorm_launch(c->xs, D32(o_last), n_req, d, c->fnorm, m.rms_eps, c->a, s));
+  float* lg = logits;
+  if (!lg) {
+    if (c->logits_rows < n_req) {
+      if (c->logits) cudaFree(c->logits);
+      c->logits = dev_alloc<float>(static_cast<size_t>(n_req) * m.vocab, &e);
+      if (e != cudaSuccess) { c->logits = nullptr; c->logits_rows = 0; return fail(RC_E_NOMEM, "logits buffer"); }
+      c->logits_rows = n_req;
+    }
+    lg = c->logits;
+  }
+  EpiArgs el{};
+  el.out = lg; el.ldo = m.vocab;
+  RC_LAUNCH(RC_K_LMHEAD, gemm_flops(n_req, m.vocab, d), gemm_bytes(n_req, m.vocab, d, 4), -1,
+            gemm_launch(&c->mA_a, &c->mB_lm, n_req, m.vocab, d, c->bn_lm, EPI_F32, el, c->num_sms, s));
+  if (cand_scores && n_cand > 0)
+    RC_LAUNCH(RC_K_SMALL, 0, n_cand * 12.0, -1,
+              cand_scores_launch(lg, m.vocab, D32(o_creq), D32(o_cid), n_cand, cand_scores, s));
+  if (c->prof) {  // Sel positions are chosen on the device: fetch them to count attention flops
+    rc_ctx::Pending pd;
+    pd.S = S;
+    pd.layers = L - cL;
+    if (cudaMallocHost(&pd.host, static_cast<size_t>(S) * 4) != cudaSuccess) return fail(RC_E_NOMEM, "profile buffer");
+    RC_CUDA(cudaMemcpyAsync(pd.host, c->sel_pos, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
+    c->pend.push_back(std::move(pd));
+  }
+  if (sel_pos_out) RC_CUDA(cudaMemcpyAsync(sel_pos_out, c->sel_pos, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToDevice, s));
+  if (hidden) RC_CUDA(cudaMemcpyAsync(hidden, c->xs, static_cast<size_t>(S) * d * 4, cudaMemcpyDeviceToDevice, s));
+  return RC_OK;
+}
+
+rc_status rc_seq_read_kv(rc_ctx* c, rc_seq seq, int32_t layer, void* k_out, void* v_out, rc_stream stream) {
+  if (!c || !k_out || !v_out) return fail(RC_E_INVALID, "null argument");
+  auto it = c->seqs.find(seq);
+  if (it == c->seqs.end()) return fail(RC_E_NOTFOUND, "unknown sequence");
+  if (layer < 0 || layer >= c->m.n_layers) return fail(RC_E_INVALID, "layer out of range");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RC_LAUNCH(RC_K_SMALL, 0, 0, -1,
+            read_kv_launch(c->arena, c->pd.arena_rows, layer, c->m.n_kv_heads, c->m.head_dim,
+                           static_cast<int32_t>(it->second.arena_row), it->second.n, static_cast<uint16_t*>(k_out),
+                           static_cast<uint16_t*>(v_out), s));
+  return RC_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU
+rc_status rc_pool_export(rc_ctx* c, void* handle_out, int64_t* rows_out) {
+  if (!c || !handle_out) return fail(RC_E_INVALID, "null argument");
+  if (!c->item_pool) return fail(RC_E_INVALID, "no item pool");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  RC_CUDA(cudaIpcGetMemHandle(&h, c->item_pool));
+  std::memcpy(handle_out, &h, sizeof(h));
+  if (rows_out) *rows_out = c->pd.item_rows;
+  return RC_OK;
+}
+
+rc_status rc_peer_attach(rc_ctx* c, int32_t n, const int32_t* rank, const int32_t* peer_dev, const void* const* handles,
+                         const int64_t* rows) {
+  if (!c || n < 0 || (n > 0 && (!rank || !handles || !rows))) return fail(RC_E_INVALID, "null argument");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t own{};
+  const bool have_own = c->item_pool && cudaIpcGetMemHandle(&own, c->item_pool) == cudaSuccess;
+  for (int i = 0; i < n; ++i) {
+    if (have_own && std::memcmp(handles[i], &own, sizeof(own)) == 0) {
+      c->peers[rank[i]] = {c->item_pool, c->pd.item_rows};  // loopback
+      continue;
+    }
+    if (peer_dev) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, c->device, peer_dev[i]);
+      if (!can) return fail(RC_E_PEER, "no P2P path to peer device " + std::to_string(peer_dev[i]));
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles[i], sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(RC_E_PEER, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    c->ipc_opened.push_back(p);
+    c->peers[rank[i]] = {static_cast<const uint16_t*>(p), rows[i]};
+  }
+  return RC_OK;
+}
+
+rc_status rc_fetch_remote(rc_ctx* c, int32_t n_items, const uint64_t* ids, const int32_t* owner, const int64_t* owner_row,
+                          const int32_t* n_tokens, const int32_t* canon_pos, rc_stream stream) {
+  if (!c || n_items < 0 || (n_items > 0 && (!ids || !owner || !owner_row || !n_tokens || !canon_pos)))
+    return fail(RC_E_INVALID, "null argument");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t need = 0;
+  for (int i = 0; i < n_items; ++i) {
+    if (!c->peers.count(owner[i])) return fail(RC_E_PEER, "owner rank not attached");
+    if (n_tokens[i] <= 0 || owner_row[i] < 0) return fail(RC_E_INVALID, "bad fetch entry");
+    if (!c->items.count(ids[i])) need += n_tokens[i];
+  }
+  if (need > c->pd.remote_rows) return fail(RC_E_CAPACITY, "remote region smaller than one fetch");
+  const int64_t planes = plane_count(c);
+  const int row_bytes = c->m.head_dim * 2;
+  for (int i = 0; i < n_items; ++i) {
+    if (c->items.count(ids[i])) { c->items[ids[i]].last_use = c->use_clock; continue; }
+    int64_t row = c->remote_alloc.alloc(n_tokens[i]);
+    while (row < 0) {  // evict least-recently used remote items (not used by this call)
+      uint64_t victim = 0, best = ~0ull;
+      for (auto& kv : c->items)
+        if (kv.second.remote && kv.second.last_use < best && kv.second.last_use != c->use_clock) {
+          best = kv.second.last_use;
+          victim = kv.first;
+        }
+      if (best == ~0ull) return fail(RC_E_CAPACITY, "remote region exhausted");
+      const Block b = c->items[victim];
+      c->remote_alloc.release(b.row - (c->pd.item_rows - c->pd.remote_rows), b.n);
+      c->items.erase(victim);
+      row = c->remote_alloc.alloc(n_tokens[i]);
+    }
+    const int64_t grow = (c->pd.item_rows - c->pd.remote_rows) + row;
+    const auto& peer = c->peers[owner[i]];
+    RC_LAUNCH(RC_K_FETCH, 0, 2.0 * planes * n_tokens[i] * row_bytes, -1,
+              copy_rows_launch(peer.first, peer.second, owner_row[i], c->item_pool, c->pd.item_rows, grow, n_tokens[i],
+                               static_cast<int32_t>(planes), row_bytes, s));
+    c->items[ids[i]] = Block{grow, n_tokens[i], canon_pos[i], true, c->use_clock};
+  }
+  return RC_OK;
+}
+
+// ------------------------------------------------------------------ profiling
+rc_status rc_profile_begin(rc_ctx* c) {
+  if (!c) return fail(RC_E_INVALID, "null ctx");
+  c->prof = true;
+  c->recs.clear();
+  c->ev_used = 0;
+  for (auto& p : c->pend) cudaFreeHost(p.host);
+  c->pend.clear();
+  return RC_OK;
+}
+
+rc_status rc_profile_end(rc_ctx* c, int32_t n_kinds, double* ms, int64_t* count, double* flops, double* bytes) {
+  if (!c || n_kinds <= 0 || !ms || !count || !flops || !bytes) return fail(RC_E_INVALID, "null argument");
+  RC_CUDA(cudaSetDevice(c->device));
+  RC_CUDA(cudaDeviceSynchronize());
+  std::vector<double> pend_flops(c->pend.size(), 0.0);
+  for (size_t i = 0; i < c->pend.size(); ++i) {
+    double sum = 0;
+    for (int j = 0; j < c->pend[i].S; ++j) sum += c->pend[i].host[j] + 1.0;
+    pend_flops[i] = 4.0 * c->m.n_heads * c->m.head_dim * sum;
+  }
+  for (int k = 0; k < n_kinds; ++k) { ms[k] = 0; count[k] = 0; flops[k] = 0; bytes[k] = 0; }
+  for (auto& r : c->recs) {
+    if (r.kind >= n_kinds) continue;
+    float t = 0;
+    RC_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.kind] += t;
+    count[r.kind] += 1;
+    flops[r.kind] += r.pending >= 0 && r.pending < static_cast<int>(pend_flops.size()) ? pend_flops[r.pending] : r.flops;
+    bytes[r.kind] += r.bytes;
+  }
+  c->prof = false;
+  c->recs.clear();
+  c->ev_used = 0;
+  for (auto& p : c->pend) cudaFreeHost(p.host);
+  c->pend.clear();
+  return RC_OK;
+}
+
+// ------------------------------------------------------------------ diagnostics
+rc_status rc_diag_gemm(int32_t M, int32_t N, int32_t K, const void* A, const void* B, float* C, int32_t bn,
+                       rc_stream stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C || (bn != 128 && bn != 256)) return fail(RC_E_INVALID, "bad gemm args");
+  CUtensorMap ma, mb;
+  if (!make_tmap_bf16_2d(&ma, A, M, K, K, 128) || !make_tmap_bf16_2d(&mb, B, N, K, K, bn))
+    return fail(RC_E_CUDA, "tensor map encode failed");
+  int dev = 0, sms = 148;
+  RC_CUDA(cudaGetDevice(&dev));
+  RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  EpiArgs ep{};
+  ep.out = C; ep.ldo = N;
+  RC_CUDA(gemm_launch(&ma, &mb, M, N, K, bn, EPI_F32, ep, sms, static_cast<cudaStream_t>(stream)));
+  return RC_OK;
+}
+
+rc_status rc_diag_deviation_select(int32_t n_u, int32_t width, const void* k_new, const void* k_st, const void* v_new,
+                                   const void* v_st, const uint8_t* cls_host, int32_t prefix_len, int32_t r_rev_bp,
+                                   int32_t r_item_bp, int32_t window, uint64_t* dev_out, int32_t* sel_out,
+                                   int32_t* n_sel_out, rc_stream stream) {
+  if (n_u <= 0 || n_u > 8192 || width <= 0 || !k_new || !k_st || !v_new || !v_st || !cls_host || !dev_out || !sel_out ||
+      !n_sel_out || prefix_len < 0 || prefix_len + n_u > 8192)
+    return fail(RC_E_INVALID, "bad diag args");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = prefix_len + n_u;
+  int nh = 0, ni = 0, nf = 0;
+  for (int i = 0; i < n_u; ++i) {
+    const int pos = prefix_len + i;
+    if (window > 0 && pos >= n - window) { ++nf; continue; }
+    nh += cls_host[i] == RC_TOK_HIST; ni += cls_host[i] == RC_TOK_ITEM; nf += cls_host[i] == RC_TOK_FORCED;
+  }
+  const int kh = budget(r_rev_bp, nh), ki = budget(r_item_bp, ni);
+  const int cnt = nf + kh + ki;
+  uint8_t* dcls = nullptr;
+  int4* dreq = nullptr;
+  int32_t *dp = nullptr, *dd = nullptr, *du = nullptr;
+  RC_CUDA(cudaMalloc(&dcls, n_u));
+  RC_CUDA(cudaMalloc(&dreq, 32));
+  RC_CUDA(cudaMalloc(&dp, std::max(cnt, 1) * 4));
+  RC_CUDA(cudaMalloc(&dd, std::max(cnt, 1) * 4));
+  RC_CUDA(cudaMalloc(&du, std::max(cnt, 1) * 4));
+  int4 hreq[2] = {make_int4(0, n_u, 0, n), make_int4(kh, ki, 0, window)};
+  RC_CUDA(cudaMemcpyAsync(dcls, cls_host, n_u, cudaMemcpyHostToDevice, s));
+  RC_CUDA(cudaMemcpyAsync(dreq, hreq, 32, cudaMemcpyHostToDevice, s));
+  RC_CUDA(dev_diag_launch(static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(k_st),
+                          static_cast<const uint16_t*>(v_new), static_cast<const uint16_t*>(v_st), n_u, width,
+                          reinterpret_cast<unsigned long long*>(dev_out), s));
+  SelectArgs sa{};
+  sa.dev = reinterpret_cast<const unsigned long long*>(dev_out);
+  sa.ucls = dcls; sa.req = dreq; sa.req2 = dreq + 1; sa.n_req = 1;
+  sa.sel_pos = dp; sa.sel_dst = dd; sa.sel_urow = du;
+  RC_CUDA(select_launch(sa, s));
+  RC_CUDA(cudaMemcpyAsync(sel_out, dp, cnt * 4, cudaMemcpyDeviceToDevice, s));
+  RC_CUDA(cudaStreamSynchronize(s));
+  cudaFree(dcls); cudaFree(dreq); cudaFree(dp); cudaFree(dd); cudaFree(du);
+  *n_sel_out = cnt;
+  return RC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// Internal launcher declarations of librc (not part of the C-ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rc {
+
+// ---------------------------------------------------------------- dense GEMM (tcgen05, k_gemm.cu)
+// C[M][N] = A[M][K] * B[N][K]^T, A and B bf16 K-major, fp32 accumulation in TMEM; the epilogue
+// decides what happens to each fp32 accumulator row.
+enum EpiKind : int {
+  EPI_BF16 = 0,     // out bf16 [M][ldo] (= acc + bias)
+  EPI_F32 = 1,      // out f32  [M][ldo]
+  EPI_ADD_F32 = 2,  // out f32  [M][ldo] += acc (residual stream)
+  EPI_SWIGLU = 3,   // N-tile = [128 gate | 128 up] -> out bf16 [M][ldo] = silu(g) * u
+  EPI_QKV = 4,      // packed [q | k | v] heads: RoPE at pos[row] on q,k; q -> q_out, k,v -> stitched arena
+  EPI_DEV = 5,      // packed [k | v] heads: RoPE on k, bf16 round, fixed-point |new - stitched| -> dev[row]
+};
+
+struct EpiArgs {
+  void* out = nullptr;
+  int64_t ldo = 0;
+  const uint16_t* bias = nullptr;  // bf16 [N]
+  const int32_t* pos = nullptr;    // [M] token positions (QKV/DEV)
+  const int32_t* dst_row = nullptr;  // [M] stitched-arena rows (QKV/DEV)
+  uint16_t* q_out = nullptr;
+  int64_t q_ld = 0;
+  uint16_t* arena_k = nullptr;  // layer base of K heads: [Hk][T_cap][dh]
+  uint16_t* arena_v = nullptr;
+  int64_t head_stride = 0;      // T_cap * dh
+  const float* rope_cos = nullptr;  // [(2*rope_zero+1)][dh/2]
+  const float* rope_sin = nullptr;
+  int32_t rope_zero = 0;
+  int32_t n_heads = 0, n_kv_heads = 0, head_dim = 0;
+  unsigned long long* dev_out = nullptr;  // [M]
+  const uint8_t* row_reuse = nullptr;     // [M]
+};
+
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                       uint32_t box_rows);
+cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, int M, int N, int K, int bn, int epi,
+                        const EpiArgs& ep, int num_sms, cudaStream_t s);
+int gemm_box_rows_b(int bn);
+
+// ---------------------------------------------------------------- assemble gather (k_gather.cu)
+struct GatherArgs {
+  const int4* meta;      // per token {dst_row, src_row, delta, kind}
+  int32_t n_tok;
+  int32_t layer_begin, layer_end;
+  int32_t n_kv_heads, head_dim;
+  const uint16_t* item_pool; int64_t item_rows;     // [L][2][Hk][item_rows][dh]
+  const int8_t* hist_q; const float* hist_s; int64_t hist_rows;  // [L][2][Hk][rows][dh], [L][2][Hk][rows]
+  const uint16_t* prefix_pool; int64_t prefix_rows;
+  uint16_t* arena; int64_t arena_rows;
+  const float* rope_cos; const float* rope_sin; int32_t rope_zero;
+};
+cudaError_t gather_launch(const GatherArgs& g, int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- attention (k_attn.cu)
+struct AttnArgs {
+  const uint16_t* q;    // [R][H*dh]
+  uint16_t* o;          // [R][H*dh]
+  const int32_t* qpos;  // [R]
+  const int4* tiles;    // {row_start, n_rows, kv_base_row, 0}
+  int32_t n_tiles;
+  const uint16_t* k;    // layer base [Hk][T_cap][dh]
+  const uint16_t* v;
+  int64_t head_stride;  // T_cap*dh
+  int32_t n_heads, n_kv_heads, head_dim;
+  float scale_log2;     // log2(e)/sqrt(dh)
+};
+int attn_tokens_per_tile(int group);
+cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- small kernels (k_small.cu)
+cudaError_t embed_launch(const uint16_t* emb, const int32_t* tok, int32_t rows, int32_t d, float* x, cudaStream_t s);
+cudaError_t rmsnorm_launch(const float* x, const int32_t* row_idx, int32_t rows, int32_t d, const uint16_t* g,
+                           float eps, uint16_t* out, cudaStream_t s);
+cudaError_t gather_rows_f32_launch(const float* src, const int32_t* idx, int32_t rows, int32_t d, float* dst,
+                                   cudaStream_t s);
+struct SelectArgs {
+  const unsigned long long* dev;  // [U rows]
+  const uint8_t* ucls;            // [U rows] class of every U row
+  const int4* req;                // per request {u_off, u_cnt, sel_off, n}  (prefix length = n - u_cnt)
+  const int4* req2;               // per request {k_hist, k_item, arena_base, window}
+  int32_t n_req;
+  int32_t* sel_pos; int32_t* sel_dst; int32_t* sel_urow;
+};
+cudaError_t dev_diag_launch(const uint16_t* kn, const uint16_t* ks, const uint16_t* vn, const uint16_t* vs, int32_t n,
+                            int32_t width, unsigned long long* out, cudaStream_t s);
+cudaError_t select_launch(const SelectArgs& a, cudaStream_t s);
+cudaError_t cand_scores_launch(const float* logits, int64_t vocab, const int32_t* cand_req, const int32_t* idtok,
+                               int32_t n, float* out, cudaStream_t s);
+cudaError_t pool_transpose_launch(const void* src, int elem_bytes, int32_t n_tok, int32_t L, int32_t Hk,
+                                  int32_t dh, void* dst, int64_t dst_rows, int64_t dst_row0, cudaStream_t s);
+cudaError_t scale_transpose_launch(const float* src, int32_t n_tok, int32_t L, int32_t Hk, float* dst,
+                                   int64_t dst_rows, int64_t dst_row0, cudaStream_t s);
+cudaError_t copy_rows_launch(const void* src_base, int64_t src_rows, int64_t src_row0, void* dst_base,
+                             int64_t dst_rows, int64_t dst_row0, int32_t n_rows, int32_t n_planes,
+                             int32_t row_bytes, cudaStream_t s);
+cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
+                           int32_t row0, int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s);
+
+}  // namespace rc

@@ -99,9 +99,18 @@ def gen_system_prompt(wl: Workload, seed: int = 3) -> np.ndarray:
     return rng.integers(0, _free_vocab(wl), size=wl.prefix_len).astype(np.int32)
 
 
+_ZIPF_CDF = {}
+
+
 def _zipf_pick(rng, m: int, s: float) -> int:
-    w = 1.0 / np.power(np.arange(1, m + 1, dtype=np.float64), s)
-    return int(rng.choice(m, p=w / w.sum()))
+    """Same draw as rng.choice(m, p=zipf weights): one uniform, searched in the cdf."""
+    cdf = _ZIPF_CDF.get((m, s))
+    if cdf is None:
+        w = 1.0 / np.power(np.arange(1, m + 1, dtype=np.float64), s)
+        cdf = np.cumsum(w / w.sum())
+        cdf /= cdf[-1]
+        _ZIPF_CDF[(m, s)] = cdf
+    return int(cdf.searchsorted(rng.random(), side="right"))
 
 
 def gen_request(wl: Workload, cat: Catalog, protos: Protos, i: int) -> Request:

@@ -1,0 +1,187 @@
+"""CUDA path (through the C-ABI) vs the oracle, element by element on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): gather and token selection bit-exact;
+hidden states x_L[Sel], last-token logits and KV_st[L-1][Sel] within relative L2 <= 1e-2;
+identical candidate ranking where the oracle's adjacent top-11 gaps exceed 4x the measured
+logit error (R19).
+"""
+import numpy as np
+import pytest
+import torch
+
+import rcgen
+from oracle.assemble import assemble
+from oracle.layout import PREFIX, FORCED, HIST, ITEM, budget
+from oracle.model import OracleModel, full_prefill, forward
+from oracle.numerics import bf16_bits, bf16_to_f32, deviation_fixed
+from oracle.select import select_sel
+from oracle.selective import selective_prefill
+from tests.helpers import make_case, oracle_pools, layouts, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2605_07443_b200.build import build
+    build()
+
+
+def _gpu():
+    from tests import gpu_helpers
+    return gpu_helpers
+
+
+# ----------------------------------------------------------------------------- K3 GEMM unit
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (300, 384, 320, 256), (1000, 6144, 4096, 256),
+                                      (77, 144, 112, 128), (3, 1000, 4096, 256), (513, 128, 192, 128),
+                                      (129, 512, 14336, 256)])
+def test_gemm_matches_exact_matmul(M, N, K, bn):
+    from paper_2605_07443_b200.api import diag_gemm
+    g = torch.Generator(device="cpu").manual_seed(M * 7 + N)
+    A = torch.randn((M, K), generator=g).to(torch.bfloat16)
+    B = (torch.randn((N, K), generator=g) / K ** 0.5).to(torch.bfloat16)
+    C = diag_gemm(A.cuda(), B.cuda(), bn=bn).cpu().double().numpy()
+    ref = A.double().numpy() @ B.double().numpy().T
+    assert rel_l2(C, ref) < 3e-5                     # fp32 accumulation over K (<= 14336) only
+    assert np.max(np.abs(C - ref)) < 1e-3 * np.max(np.abs(ref)) + 1e-6
+
+
+# ----------------------------------------------------------------------------- K2 gather
+@pytest.mark.parametrize("wl,gather_from", [(rcgen.CFG1, 1), (rcgen.CFG1_Q7, 1), (rcgen.CFG1, 0)])
+def test_gather_bitexact(wl, gather_from):
+    G = _gpu()
+    case = make_case(wl, n_req=2)
+    pools = oracle_pools(case)
+    ctx, _ = G.make_ctx(case, pools, 2 * wl.n)
+    lays = G.gpu_layouts(ctx, case)
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=gather_from)
+    torch.cuda.synchronize()
+    for r, lay in enumerate(layouts(case)):
+        K, V, dfn = assemble(case["shape"], lay, pools["items"], pools["hist"], pools["prefix"], gather_from)
+        for l in range(case["shape"].n_layers):
+            k, v = ctx.read_kv(seqs[r], l, lay.n)
+            kb, vb = G.bits(k), G.bits(v)
+            m = dfn[l]
+            assert m.sum() > 0
+            assert np.array_equal(kb[m], K[l][m]), f"K mismatch layer {l}"
+            assert np.array_equal(vb[m], V[l][m]), f"V mismatch layer {l}"
+    ctx.release(seqs)
+    ctx.close()
+
+
+# ----------------------------------------------------------------------------- K5 + K6 unit
+@pytest.mark.parametrize("n_u,width,r_bp,window", [(136, 64, 1500, 0), (3889, 2048, 1500, 0), (2353, 2048, 500, 0),
+                                                   (1000, 256, 3000, 17), (64, 32, 10000, 0), (500, 64, 0, 0)])
+def test_deviation_and_selection_bitexact(n_u, width, r_bp, window):
+    from paper_2605_07443_b200.api import diag_deviation_select
+    rng = np.random.default_rng(n_u + width)
+    P = 207 if n_u > 200 else 8
+    cls = rng.choice([HIST, ITEM, FORCED], size=n_u, p=[0.2, 0.75, 0.05]).astype(np.uint8)
+    cls[-5:] = FORCED
+    mk = lambda: bf16_bits(rng.standard_normal((n_u, width)).astype(np.float32))
+    kn, ks, vn, vs = mk(), mk(), mk(), mk()
+    # some exact ties in D: copy a few rows so equal deviations must fall back to position order
+    for a, b in [(3, 9), (10, 40), (41, 42)]:
+        if b < n_u:
+            kn[b], ks[b], vn[b], vs[b] = kn[a], ks[a], vn[a], vs[a]
+    ks[5], vs[5] = kn[5], vn[5]                       # zero deviation row
+    t = lambda a: torch.from_numpy(a.view(np.int16)).cuda()
+    D, sel = diag_deviation_select(t(kn), t(ks), t(vn), t(vs), cls, P, r_bp, r_bp, window)
+    Dref = deviation_fixed(bf16_to_f32(kn), bf16_to_f32(ks)) + deviation_fixed(bf16_to_f32(vn), bf16_to_f32(vs))
+    assert np.array_equal(D, Dref)
+    full_cls = np.concatenate([np.full(P, PREFIX, np.uint8), cls])
+    full_D = np.concatenate([np.zeros(P, np.uint64), Dref])
+    ref = select_sel(full_cls, full_D, r_bp, r_bp, window)
+    assert np.array_equal(sel, ref)
+
+
+# ----------------------------------------------------------------------------- end to end
+def _run_gpu(wl, case, pools, r_bp, c=1, forced=None, no_prefix=False, hidden=True, window=0):
+    G = _gpu()
+    n_tok = sum(l.n for l in layouts(case))
+    ctx, _ = G.make_ctx(case, pools, n_tok)
+    lays = G.gpu_layouts(ctx, case)
+    if no_prefix:
+        for lay in lays:
+            lay["cls"] = np.full_like(lay["cls"], FORCED)
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=c)
+    n_cand = sum(len(l["cand_idtok"]) for l in lays)
+    out = ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, window=window, forced_sel=forced, hidden=hidden,
+                                n_cand=n_cand)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
+    res["kv_last"] = [tuple(G.bits(t) for t in ctx.read_kv(s, wl.shape.n_layers - 1, lay["tokens"].shape[0]))
+                      for s, lay in zip(seqs, lays)]
+    res["launches"] = ctx.launch_count()
+    ctx.release(seqs)
+    ctx.close()
+    return res, lays
+
+
+@pytest.mark.parametrize("wl", [rcgen.CFG1, rcgen.CFG1_Q7])
+def test_full_prefill_no_prefix_matches_ofull(wl):
+    case = make_case(wl)
+    pools = oracle_pools(case)
+    res, lays = _run_gpu(wl, case, pools, 10000, no_prefix=True)
+    m = OracleModel(case["shape"], case["W"])
+    ref = full_prefill(m, lays[0]["tokens"].tolist())
+    assert rel_l2(res["logits"][0], ref["logits_last"]) < TOL
+    assert rel_l2(res["hidden"], ref["x"]) < TOL
+    assert list(res["sel_pos"]) == list(range(wl.n))
+    K = bf16_to_f32(res["kv_last"][0][0]).astype(np.float64)
+    assert rel_l2(K, ref["K"][-1]) < TOL
+
+
+def _oracle_forced(case, pools, lay, sel, r_bp, c=1, window=0):
+    m = OracleModel(case["shape"], case["W"])
+    K, V, _ = assemble(case["shape"], lay, pools["items"], pools["hist"], pools["prefix"], gather_from=c)
+    forced = selective_prefill(m, lay, K, V, r_bp, r_bp, check_layer=c, window=window, forced_sel=sel)
+    own = selective_prefill(m, lay, K, V, r_bp, r_bp, check_layer=c, window=window)
+    return forced, own
+
+
+@pytest.mark.parametrize("wl,r_bp,c", [(rcgen.CFG1, 1500, 1), (rcgen.CFG1_Q7, 1500, 1), (rcgen.CFG1, 3000, 0),
+                                       (rcgen.CFG1, 10000, 1), (rcgen.CFG1, 0, 1)])
+def test_selective_prefill_parity(wl, r_bp, c):
+    case = make_case(wl)
+    pools = oracle_pools(case)
+    res, lays = _run_gpu(wl, case, pools, r_bp, c=c)
+    lay = layouts(case)[0]
+    sel = res["sel_pos"]
+    assert len(sel) == len(set(sel.tolist())) and list(sel) == sorted(sel)
+    assert set(np.nonzero(lay.cls == FORCED)[0]) <= set(sel.tolist())
+    forced, own = _oracle_forced(case, pools, lay, sel, r_bp, c)
+    # selection: same budgets; Jaccard vs the oracle's own choice (bf16 noise may flip near-ties)
+    assert len(own["sel"]) == len(sel)
+    jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
+    assert jac >= 0.8, jac
+    assert rel_l2(res["logits"][0], forced["logits"]) < TOL
+    assert rel_l2(res["hidden"], forced["x_sel"]) < TOL
+    L = case["shape"].n_layers
+    Kg = bf16_to_f32(res["kv_last"][0][0])[sel].astype(np.float64)
+    Vg = bf16_to_f32(res["kv_last"][0][1])[sel].astype(np.float64)
+    assert rel_l2(Kg, forced["K"][L - 1][sel]) < TOL and rel_l2(Vg, forced["V"][L - 1][sel]) < TOL
+    # non-selected reused positions keep the gathered bytes at the last layer
+    K_asm, V_asm, dfn = assemble(case["shape"], lay, pools["items"], pools["hist"], pools["prefix"], gather_from=c)
+    keep = np.array([p for p in range(lay.n) if p not in set(sel.tolist()) and dfn[L - 1, p]])
+    if len(keep):
+        assert np.array_equal(res["kv_last"][0][0][keep], K_asm[L - 1][keep])
+    assert np.allclose(res["cand_scores"], forced["cand_scores"], rtol=0.05, atol=0.05 * np.abs(forced["cand_scores"]).max())
+
+
+def test_ragged_batch_matches_per_request():
+    wl = rcgen.CFG1
+    case = make_case(wl, n_req=3)
+    pools = oracle_pools(case)
+    res, lays = _run_gpu(wl, case, pools, 1500)
+    off = res["sel_off"]
+    for r, lay in enumerate(layouts(case)):
+        sel = res["sel_pos"][off[r]:off[r + 1]]
+        forced, _ = _oracle_forced(case, pools, lay, sel, 1500)
+        assert rel_l2(res["logits"][r], forced["logits"]) < TOL
+        assert rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
