@@ -353,13 +353,13 @@ def run_ours(args, wl):
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for i in range(args.steps):
+    for i in range(0 if args.profile_only else args.steps):
         step(args.warmup + i)
         pin_l.copy_(out_bufs["logits"], non_blocking=True)
         pin_c.copy_(out_bufs["cand_scores"], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize(device)
-    te = torch.tensor([e0.elapsed_time(e1)], device=device)
+    te = torch.tensor([max(e0.elapsed_time(e1), 1e-6)], device=device)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = tokens_all / (float(te.item()) / 1e3)
@@ -471,6 +471,9 @@ def baselines(args, wl, env, r_bp, c, step_ms):
 
 def main():
     args = parse()
+    if os.environ.get("RC_WATCHDOG"):
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["RC_WATCHDOG"]), exit=True)
     import rcgen
     wl = rcgen.WORKLOADS[args.config]
     if args.impl == "reference":

@@ -4,6 +4,7 @@
 // launch order only.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -198,6 +199,11 @@ struct rc_ctx {
   CUtensorMap mA_a{}, mA_o{}, mA_h{};
   std::vector<CUtensorMap> mB_qkv, mB_kv, mB_o, mB_gu, mB_d;
   CUtensorMap mB_lm{};
+  bool attn_tc = false;                 // tcgen05 attention (head_dim 128)
+  CUtensorMap mQ3{};                    // q workspace as [R][H][dh]
+  std::vector<CUtensorMap> mK_att, mV_att;  // arena K / V per layer as [Hk*T_cap][dh]
+  int attn_tq() const { return attn_tc ? attn_tc_tokens_per_tile(m.n_heads / m.n_kv_heads)
+                                       : attn_tokens_per_tile(m.n_heads / m.n_kv_heads); }
   int bn_qkv = 256, bn_kv = 256, bn_o = 256, bn_d = 256, bn_lm = 256;
   Staging stage;
   int64_t launches = 0;
@@ -364,6 +370,9 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   }
   c->arena = dev_alloc<uint16_t>(static_cast<size_t>(planes) * std::max<int64_t>(pd->arena_rows, 1) * dh, &e);
   if (e != cudaSuccess) return fail(RC_E_NOMEM, "stitched-KV arena");
+  // every arena byte stays a finite bf16 (attention tiles may read rows past a request's end; they are
+  // masked, and 0 * finite = 0 inside P V)
+  RC_CUDA(cudaMemset(c->arena, 0, static_cast<size_t>(planes) * std::max<int64_t>(pd->arena_rows, 1) * dh * 2));
   c->arena_alloc.init(pd->arena_rows);
   rc_status st = build_rope(c.get());
   if (st != RC_OK) return st;
@@ -399,6 +408,20 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
     ok = ok && make_tmap_bf16_2d(&c->mB_d[l], c->wd[l], d, F, F, c->bn_d);
   }
   ok = ok && make_tmap_bf16_2d(&c->mB_lm, c->lm_head, m.vocab, d, d, c->bn_lm);
+  c->attn_tc = (dh == 128) && std::getenv("RC_ATTN_LEGACY") == nullptr;
+  if (c->attn_tc && ok) {
+    const int G = H / Hk;
+    const int TQ = attn_tc_tokens_per_tile(G);
+    ok = make_tmap_bf16_3d(&c->mQ3, c->q, dh, H, Mx, static_cast<uint64_t>(dh) * 2, static_cast<uint64_t>(H) * dh * 2,
+                           64, G, TQ);
+    c->mK_att.resize(L); c->mV_att.resize(L);
+    for (int l = 0; l < L && ok; ++l) {
+      ok = make_tmap_bf16_2d(&c->mK_att[l], arena_layer(c.get(), l, 0), static_cast<uint64_t>(Hk) * pd->arena_rows, dh,
+                             dh, 128) &&
+           make_tmap_bf16_2d(&c->mV_att[l], arena_layer(c.get(), l, 1), static_cast<uint64_t>(Hk) * pd->arena_rows, dh,
+                             dh, 128);
+    }
+  }
   if (!ok) return fail(RC_E_CUDA, "cuTensorMapEncodeTiled failed (driver entry point or alignment)");
   RC_CUDA(cudaDeviceSynchronize());
   *out = c.release();
@@ -746,7 +769,11 @@ rc_status run_layer(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_p
   at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
   at.n_heads = H; at.n_kv_heads = Hk; at.head_dim = dh;
   at.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
-  RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending, attn_launch(at, s));
+  if (c->attn_tc)
+    RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
+              attn_tc_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
+  else
+    RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending, attn_launch(at, s));
   EpiArgs eo{};
   eo.out = x; eo.ldo = d;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, H * dh), gemm_bytes(R, d, H * dh, 8), -1,
@@ -774,7 +801,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   if (st != RC_OK) return st;
   const rc_model_desc& m = c->m;
   const int L = m.n_layers, d = m.d_model, cL = prm->check_layer;
-  const int TQ = attn_tokens_per_tile(m.n_heads / m.n_kv_heads);
+  const int TQ = c->attn_tq();
   const int32_t U = plan.back().u_off + plan.back().u_cnt;
   const int32_t S = plan.back().sel_off + plan.back().sel_cnt;
   int32_t n_cand = 0;

@@ -72,6 +72,13 @@ struct AttnArgs {
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
+// tcgen05 version (head_dim == 128): 128-row tiles, Q via a 3-D tensor map over q [R][H][dh],
+// K/V via 2-D maps over the layer's arena [Hk*T_cap][dh] (k_attn_tc.cu)
+int attn_tc_tokens_per_tile(int group);
+cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV, const AttnArgs& a,
+                           int64_t t_cap, cudaStream_t s);
+bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+                       uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 
 // ---------------------------------------------------------------- small kernels (k_small.cu)
 cudaError_t embed_launch(const uint16_t* emb, const int32_t* tok, int32_t rows, int32_t d, float* x, cudaStream_t s);

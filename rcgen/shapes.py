@@ -45,7 +45,12 @@ TINY_Q7 = ModelShape("tiny-q7", 2, 112, 7, 1, 16, 256, 512, 1e6, 1e-6, True)
 LLAMA3_8B = ModelShape("llama3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 5e5, 1e-5, False)
 QWEN2_7B = ModelShape("qwen2-7b", 28, 3584, 28, 4, 128, 18944, 152064, 1e6, 1e-6, True)
 
-SHAPES = {s.name: s for s in (TINY, TINY_Q7, LLAMA3_8B, QWEN2_7B)}
+# mini test shapes with the real head geometry (d_h = 128, GQA 4 / GQA 7 + bias) so that the
+# tcgen05 attention and multi-tile paths run at sizes the oracle finishes in seconds.
+MINI_LLAMA = ModelShape("mini-llama", 3, 1024, 8, 2, 128, 2048, 4096, 5e5, 1e-5, False)
+MINI_QWEN = ModelShape("mini-qwen", 3, 896, 7, 1, 128, 2048, 4096, 1e6, 1e-6, True)
+
+SHAPES = {s.name: s for s in (TINY, TINY_Q7, LLAMA3_8B, QWEN2_7B, MINI_LLAMA, MINI_QWEN)}
 
 
 @dataclass(frozen=True)
@@ -76,6 +81,9 @@ CFG2 = Workload("cfg2-llama-1k", LLAMA3_8B, 207, 1024, 20, 64, 49, 4096, 256, 10
 CFG3 = Workload("cfg3-llama-4k", LLAMA3_8B, 207, 640, 50, 64, 49, 4096, 256, 100_000, 32)
 CFG5 = Workload("cfg5-qwen-8k", QWEN2_7B, 207, 1536, 100, 64, 49, 8192, 256, 100_000, 1)
 
-WORKLOADS = {w.name: w for w in (CFG1, CFG1_Q7, CFG2, CFG3, CFG5)}
+MINI_L = Workload("mini-llama", MINI_LLAMA, 64, 160, 8, 32, 16, 256, 16, 2048, 2)
+MINI_Q = Workload("mini-qwen", MINI_QWEN, 64, 160, 8, 32, 16, 256, 16, 2048, 2)
+
+WORKLOADS = {w.name: w for w in (CFG1, CFG1_Q7, CFG2, CFG3, CFG5, MINI_L, MINI_Q)}
 
 assert CFG1.n == 144 and CFG2.n == 2560 and CFG3.n == 4096 and CFG5.n == 8192

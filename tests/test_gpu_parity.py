@@ -52,7 +52,8 @@ def test_gemm_matches_exact_matmul(M, N, K, bn):
 
 
 # ----------------------------------------------------------------------------- K2 gather
-@pytest.mark.parametrize("wl,gather_from", [(rcgen.CFG1, 1), (rcgen.CFG1_Q7, 1), (rcgen.CFG1, 0)])
+@pytest.mark.parametrize("wl,gather_from", [(rcgen.CFG1, 1), (rcgen.CFG1_Q7, 1), (rcgen.CFG1, 0), (rcgen.MINI_L, 1),
+                                             (rcgen.MINI_Q, 2)])
 def test_gather_bitexact(wl, gather_from):
     G = _gpu()
     case = make_case(wl, n_req=2)
@@ -123,7 +124,7 @@ def _run_gpu(wl, case, pools, r_bp, c=1, forced=None, no_prefix=False, hidden=Tr
     return res, lays
 
 
-@pytest.mark.parametrize("wl", [rcgen.CFG1, rcgen.CFG1_Q7])
+@pytest.mark.parametrize("wl", [rcgen.CFG1, rcgen.CFG1_Q7, rcgen.MINI_L, rcgen.MINI_Q])
 def test_full_prefill_no_prefix_matches_ofull(wl):
     case = make_case(wl)
     pools = oracle_pools(case)
@@ -146,7 +147,8 @@ def _oracle_forced(case, pools, lay, sel, r_bp, c=1, window=0):
 
 
 @pytest.mark.parametrize("wl,r_bp,c", [(rcgen.CFG1, 1500, 1), (rcgen.CFG1_Q7, 1500, 1), (rcgen.CFG1, 3000, 0),
-                                       (rcgen.CFG1, 10000, 1), (rcgen.CFG1, 0, 1)])
+                                       (rcgen.CFG1, 10000, 1), (rcgen.CFG1, 0, 1), (rcgen.MINI_L, 1500, 1),
+                                       (rcgen.MINI_Q, 1500, 1), (rcgen.MINI_L, 3000, 2), (rcgen.MINI_Q, 10000, 1)])
 def test_selective_prefill_parity(wl, r_bp, c):
     case = make_case(wl)
     pools = oracle_pools(case)
