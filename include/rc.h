@@ -194,6 +194,26 @@ rc_status rc_selective_prefill(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, c
 void rc_release(rc_ctx* ctx, int32_t n, const rc_seq* seqs);
 
 /* ---------------------------------------------------------------- multi-GPU (§8(e)) */
+/* Alg. 1 similarity-aware item placement with global replicas, host only.
+ * Phase 1 heat h_i = occurrences of item i in the historical requests (CSR hist_off [n_hist+1] /
+ * hist_items); Phase 2 the top ceil(hot_bp/10000 * n_items) items by heat (ties -> smaller id)
+ * are replicated on all k instances (part_out = -1); Phases 3-5 the cold items form a graph with
+ * edge weight = number of historical requests in which both occur, partitioned k ways
+ * minimising the edge cut with every part's token weight (item_tokens) <= (1+eps) * total/k
+ * (multilevel heavy-edge coarsening + greedy + boundary refinement, `passes` per level; a
+ * self-contained stand-in for METIS). Outputs: part_out [n_items] in -1..k-1, edge cut,
+ * heat_out [n_items] (may be NULL). Deterministic. Errors: INVALID. */
+rc_status rc_place_items(int32_t n_items, const int32_t* item_tokens, int32_t n_hist, const int64_t* hist_off,
+                         const int32_t* hist_items, int32_t k, int32_t hot_bp, double balance_eps, int32_t passes,
+                         int32_t* part_out, int64_t* cut_out, int64_t* heat_out);
+/* Eq. 2 affinity routing, host only, requests in arrival order:
+ * Affinity(R,p) = alpha * |I(R) n C(p)|/|I(R)| + beta * (1 - Load(p)), Load(p) = backlog[p] /
+ * max(1, max_q backlog[q]) (queue tokens); route = argmax, ties -> smaller p;
+ * the chosen backlog grows by req_tokens[r]. C(p) = resident[p * n_items + i] != 0.
+ * backlog [k] is read and updated in place. Errors: INVALID (empty request, id out of range). */
+rc_status rc_route(int32_t n_req, const int64_t* req_off, const int32_t* req_items, const int64_t* req_tokens,
+                   int32_t k, int32_t n_items, const uint8_t* resident, double alpha, double beta, int64_t* backlog,
+                   int32_t* route_out);
 /* Export the item pool allocation as a CUDA IPC handle (64 bytes) for peers. */
 rc_status rc_pool_export(rc_ctx* ctx, void* ipc_handle_out, int64_t* pool_rows_out);
 /* Map peers' item pools (one-sided NVLink reads). rank = the peer's index used in

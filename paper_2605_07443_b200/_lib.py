@@ -94,6 +94,10 @@ def lib():
                                                      C.c_int32, C.c_int32, P, P, I32P, P]),
             "rc_diag_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int32, P]),
             "rc_launch_count": (C.c_int64, [P]),
+            "rc_place_items": (C.c_int32, [C.c_int32, I32P, C.c_int32, I64P, I32P, C.c_int32, C.c_int32, C.c_double,
+                                           C.c_int32, I32P, I64P, I64P]),
+            "rc_route": (C.c_int32, [C.c_int32, I64P, I32P, I64P, C.c_int32, C.c_int32, U8P, C.c_double, C.c_double,
+                                     I64P, I32P]),
             "rc_profile_begin": (C.c_int32, [P]),
             "rc_profile_end": (C.c_int32, [P, C.c_int32, C.POINTER(C.c_double), I64P, C.POINTER(C.c_double),
                                            C.POINTER(C.c_double)]),
@@ -120,5 +124,5 @@ EXPORTED = ["rc_create", "rc_destroy", "rc_last_error", "rc_abi_version", "rc_de
             "rc_pool_register_blocks", "rc_pool_contains", "rc_pool_locate", "rc_assemble", "rc_sel_count",
             "rc_selective_prefill", "rc_release", "rc_pool_export", "rc_peer_attach", "rc_fetch_remote",
             "rc_seq_read_kv", "rc_diag_deviation_select", "rc_diag_gemm", "rc_launch_count", "rc_profile_begin",
-            "rc_profile_end"]
+            "rc_profile_end", "rc_place_items", "rc_route"]
 KINDS = ["gemm", "attention", "gather", "select", "small", "lm_head", "fetch"]

@@ -21,15 +21,28 @@ constexpr int DH = 128, BKV = 128, ROWS = 128;
 constexpr uint32_t HALF = ROWS * 64 * 2;  // one [128 rows][64 bf16] SW128 sub-tile = 16 KB
 constexpr uint32_t TILE = 2 * HALF;       // 32 KB
 constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = 3 * TILE, OFF_P = 5 * TILE, OFF_BAR = 7 * TILE;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;
+constexpr uint32_t OFF_RED = OFF_BAR + 256;            // [2 tile slots][2 column halves][128 rows] f32
+constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
+constexpr int SCOLS = BKV / 2;                          // S columns per softmax thread (two warps per row)
+constexpr int NTHREADS = 384;                           // 4 control warps + 8 softmax warps
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 
-__global__ void __launch_bounds__(256, 1)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int64_t t_cap) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 224 KB of tiles + barriers + exchange: no room for a manual 1 KB alignment pad, so the
+  // dynamic window must itself be 1024-aligned (SWIZZLE_128B atoms); checked below.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
   uint8_t* sQ = smem + OFF_Q;
+  float* red = reinterpret_cast<float*>(smem + OFF_RED);
   uint8_t* sK = smem + OFF_K;
   uint8_t* sV = smem + OFF_V;
   uint8_t* sP = smem + OFF_P;
@@ -59,7 +72,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); mbar_init(&pv_done[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&pv_done[i], 1);
     }
     fence_barrier_init();
     fence_proxy_async();
@@ -134,79 +147,92 @@ __global__ void __launch_bounds__(256, 1)
         if (j + 2 < nkv) issue_s(j + 2);
       }
     }
-  } else if (warp >= 4) {  // ---- softmax: thread <-> row
-    const int q = warp & 3;
+  } else if (warp >= 4) {  // ---- softmax: thread <-> (row, half of the key columns)
+    const int q = warp & 3;              // TMEM lane quarter of this warp
+    const int hf = (warp - 4) >> 2;      // warps 4..7: keys 0..63 of a tile, warps 8..11: keys 64..127
+    const int col0 = hf * SCOLS;
     const int r = q * 32 + lane;
     const int t = r / G, g = r % G;
     const bool valid = (r < TQ * G) && (t < n_rows);
     const int p = valid ? a.qpos[row_start + t] : -1;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
-    uint32_t sr[BKV];
+    uint32_t sr[SCOLS];
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < BKV; c += 32) tmem_ld32(tmem + lane_base + b * 128 + c, sr + c);
+      for (int c = 0; c < SCOLS; c += 32) tmem_ld32(tmem + lane_base + b * 128 + col0 + c, sr + c);
       tmem_wait_ld();
-      const int key0 = j * BKV;
-      float mx = -INFINITY;
+      const int key0 = j * BKV + col0;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
 #pragma unroll
-      for (int c = 0; c < BKV; ++c) {
+      for (int c = 0; c < SCOLS; ++c) {
         float v = __uint_as_float(sr[c]) * a.scale_log2;
         v = (key0 + c <= p) ? v : -INFINITY;
         sr[c] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
+        mx4[c & 3] = fmaxf(mx4[c & 3], v);
       }
+      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      // combine the two column halves of this row (warp pair q+4 / q+8, named barrier 1+q)
+      red[(j & 1) * 256 + hf * 128 + r] = mx;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      mx = fmaxf(mx, red[(j & 1) * 256 + (hf ^ 1) * 128 + r]);
       float alpha = 1.f;
       bool need = false;
       if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
         const float m_new = fmaxf(m_run, mx);
-        if (m_run != -INFINITY) { alpha = exp2f(m_run - m_new); need = true; }
+        if (m_run != -INFINITY) { alpha = fast_exp2(m_run - m_new); need = true; }
         m_run = m_new;
       }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale the TMEM accumulator (rows of this warp)
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this warp's half of the TMEM accumulator rows
         mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
         uint32_t o[32];
 #pragma unroll
-        for (int c = 0; c < DH; c += 32) {
-          tmem_ld32(tmem + lane_base + 256 + c, o);
+        for (int c = 0; c < SCOLS; c += 32) {
+          tmem_ld32(tmem + lane_base + 256 + col0 + c, o);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(tmem + lane_base + 256 + c, o);
+          tmem_st32(tmem + lane_base + 256 + col0 + c, o);
         }
         tmem_wait_st();
       }
       l_run *= alpha;
       const float base = (m_run == -INFINITY) ? 0.f : m_run;
       if (j >= 2) mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);  // P buffer b free (PV_{j-2} done)
-      uint8_t* prow = sP + b * TILE + r * 128;
+      uint8_t* prow = sP + b * TILE + hf * HALF + r * 128;     // this half = one 64-key K-block of P
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int c = 0; c < BKV; c += 8) {
+      for (int c = 0; c < SCOLS; c += 8) {
         float e[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { e[i] = exp2f(__uint_as_float(sr[c + i]) - base); l_run += e[i]; }
+        for (int i = 0; i < 8; ++i) { e[i] = fast_exp2(__uint_as_float(sr[c + i]) - base); ls[i & 3] += e[i]; }
         uint4 u;
         u.x = pack_bf2(e[0], e[1]); u.y = pack_bf2(e[2], e[3]); u.z = pack_bf2(e[4], e[5]); u.w = pack_bf2(e[6], e[7]);
-        const int chunk = (c >> 3) & 7;
-        *reinterpret_cast<uint4*>(prow + (c >> 6) * HALF + ((chunk ^ (r & 7)) << 4)) = u;
+        const int chunk = c >> 3;
+        *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = u;
       }
+      l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
-    // epilogue: O / l -> bf16
+    // epilogue: O / l -> bf16 (l = sum of the two halves' partial sums)
+    // slot (nkv & 1) was last read before the final tile's barrier by both warps of the pair
+    red[(nkv & 1) * 256 + hf * 128 + r] = l_run;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    const float l_tot = l_run + red[(nkv & 1) * 256 + (hf ^ 1) * 128 + r];
     mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     tc_fence_after();
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH;
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+    uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + col0;
 #pragma unroll
-    for (int c = 0; c < DH; c += 32) {
+    for (int c = 0; c < SCOLS; c += 32) {
       uint32_t o[32];
-      tmem_ld32(tmem + lane_base + 256 + c, o);
+      tmem_ld32(tmem + lane_base + 256 + col0 + c, o);
       tmem_wait_ld();
       if (valid) {
 #pragma unroll
@@ -240,7 +266,7 @@ cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const
     attr = true;
   }
   dim3 grid(a.n_tiles, a.n_kv_heads);
-  k_attn_tc<<<grid, 256, SMEM_BYTES, s>>>(*tmQ, *tmK, *tmV, a, t_cap);
+  k_attn_tc<<<grid, NTHREADS, SMEM_BYTES, s>>>(*tmQ, *tmK, *tmV, a, t_cap);
   return cudaGetLastError();
 }
 

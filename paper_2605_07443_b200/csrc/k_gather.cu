@@ -147,7 +147,8 @@ cudaError_t launch(const GatherArgs& g, int num_sms, cudaStream_t s) {
   if (per_sm == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gather<DH>, 256, 0) != cudaSuccess)
     per_sm = 2;
   int64_t bx = (units + 256 * UNROLL - 1) / (256 * UNROLL);
-  const int64_t want = (static_cast<int64_t>(num_sms) * per_sm + planes - 1) / planes;
+  // >= 8 waves of resident CTAs in total so the per-plane tail is small
+  const int64_t want = (static_cast<int64_t>(num_sms) * per_sm * 8 + planes - 1) / planes;
   if (bx > want) bx = want;
   if (bx < 1) bx = 1;
   k_gather<DH><<<dim3(static_cast<unsigned>(bx), planes), 256, 0, s>>>(g);

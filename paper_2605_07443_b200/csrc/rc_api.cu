@@ -18,8 +18,15 @@
 using namespace rc;
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
+
+int32_t rc::set_error(int32_t code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+namespace {
 
 rc_status fail(rc_status code, const std::string& msg) {
   g_err = msg;

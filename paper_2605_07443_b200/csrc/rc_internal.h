@@ -6,6 +6,9 @@
 
 namespace rc {
 
+// sets the thread-local message returned by rc_last_error(); returns code
+int32_t set_error(int32_t code, const char* msg);
+
 // ---------------------------------------------------------------- dense GEMM (tcgen05, k_gemm.cu)
 // C[M][N] = A[M][K] * B[N][K]^T, A and B bf16 K-major, fp32 accumulation in TMEM; the epilogue
 // decides what happens to each fp32 accumulator row.
