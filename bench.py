@@ -95,7 +95,26 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload setup
-def build_ours(wl, batch, n_batches, rank, device, remote_rows=0):
+def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
+    """§8(e): Alg. 1 placement of the catalog over `world` GPUs (historical trace: 2000 seeded
+    requests), Eq. 2 routing of one global request stream; this rank keeps the requests routed
+    to it (cycled to the fixed per-GPU count: weak scaling)."""
+    import rcgen
+    from paper_2605_07443_b200 import cluster
+    hist = [r.cand_items.tolist() for r in rcgen.gen_requests(wl, cat, protos, 2000, start=5_000_000)]
+    part, cut, heat = cluster.place_items(np.full(wl.n_items, wl.item_len), hist, world, hot_bp=10)
+    res = cluster.resident_matrix(part, world)
+    stream = rcgen.gen_requests(wl, cat, protos, int(1.25 * world * batch * n_batches) + world, start=0)
+    routes, _ = cluster.route([r.cand_items.tolist() for r in stream], [wl.n] * len(stream), res)
+    mine = [r for r, p in zip(stream, routes) if p == rank] or stream[rank::world]
+    need = batch * n_batches
+    reqs = (mine * ((need + len(mine) - 1) // len(mine)))[:need]
+    hit = float(np.mean([res[rank][r.cand_items].mean() for r in reqs]))
+    return dict(part=part, cut=cut, res=res, reqs=reqs, local_hit=hit,
+                routed=[int((routes == p).sum()) for p in range(world)])
+
+
+def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None):
     import torch
     import rcgen
     from paper_2605_07443_b200.api import RcContext
@@ -104,16 +123,25 @@ def build_ours(wl, batch, n_batches, rank, device, remote_rows=0):
     shape = wl.shape
     W = rcgen.gen_weights(shape, seed=0, device=device)
     cat, protos, sys_tok = rcgen.gen_catalog(wl), rcgen.gen_protos(wl), rcgen.gen_system_prompt(wl)
-    reqs = rcgen.gen_requests(wl, cat, protos, batch * n_batches, start=rank * 1_000_000)
+    shard = None
+    if world > 1:
+        shard = shard_setup(wl, cat, protos, world, rank, batch, n_batches)
+        reqs = shard["reqs"]
+        items = np.nonzero(shard["res"][rank])[0].tolist()
+        remote_rows = batch * wl.n_cand * wl.item_len
+    else:
+        reqs = rcgen.gen_requests(wl, cat, protos, batch * n_batches, start=rank * 1_000_000)
+        items = list(range(wl.n_items))
+        remote_rows = 0
     used_protos = sorted({int(p) for r in reqs for p in r.hist_protos})
     n = wl.n
-    ctx = RcContext(shape, W, item_rows=wl.n_items * wl.item_len + remote_rows, hist_rows=wl.n_protos,
+    ctx = RcContext(shape, W, item_rows=len(items) * wl.item_len + remote_rows, hist_rows=wl.n_protos,
                     prefix_rows=wl.prefix_len, arena_rows=batch * n, max_seq_len=n, max_batch_tokens=batch * n,
                     remote_rows=remote_rows, device=device.index or 0)
-    # item pool: the whole catalog, generated on the device in chunks and registered
+    # item pool: this GPU's items (whole catalog at N=1), generated on the device in chunks and registered
     chunk = 128
-    for i0 in range(0, wl.n_items, chunk):
-        ids = list(range(i0, min(wl.n_items, i0 + chunk)))
+    for i0 in range(0, len(items), chunk):
+        ids = items[i0:i0 + chunk]
         kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
         ctx.pool_register_blocks(R.RC_POOL_ITEM_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids),
                                  kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
@@ -129,7 +157,18 @@ def build_ours(wl, batch, n_batches, rank, device, remote_rows=0):
     layouts = [ctx.decompose_prompt(sys_tok, r.hist_protos, r.hist_tokens, r.cand_items,
                                     [cat.tokens[int(i)] for i in r.cand_items], r.tail_tokens) for r in reqs]
     batches = [layouts[b * batch:(b + 1) * batch] for b in range(n_batches)]
-    return dict(ctx=ctx, W=W, cat=cat, protos=protos, sys=sys_tok, reqs=reqs, batches=batches, shape=shape)
+    fetch = None
+    if world > 1:  # NVLink: map every peer's item pool, publish the item directory, plan per-batch pulls
+        from paper_2605_07443_b200 import cluster
+        handle, rows = ctx.pool_export()
+        peers = [x for x in gather((rank, device.index, handle, rows)) if x[0] != rank]
+        ctx.peer_attach([p[0] for p in peers], [p[1] for p in peers], [p[2] for p in peers], [p[3] for p in peers])
+        directory = cluster.exchange_directory(items, ctx.pool_locate(items), rank, gather)
+        fetch = [cluster.plan_fetch([r.cand_items for r in reqs[b * batch:(b + 1) * batch]], shard["res"][rank],
+                                    directory, rank) for b in range(n_batches)]
+        shard["fetch_items_per_batch"] = float(np.mean([len(f) for f in fetch]))
+    return dict(ctx=ctx, W=W, cat=cat, protos=protos, sys=sys_tok, reqs=reqs, batches=batches, shape=shape,
+                shard=shard, fetch=fetch)
 
 
 def host_bytes(batch_layouts):
@@ -302,15 +341,25 @@ def run_ours(args, wl):
     batch = args.batch or wl.batch
     r_bp = args.r_bp or wl.r_bp
     c = args.check_layer
-    env = build_ours(wl, batch, args.distinct_batches, rank, device)
-    ctx, batches = env["ctx"], env["batches"]
+    def gather(obj):
+        lst = [None] * world
+        dist.all_gather_object(lst, obj)
+        return lst
+
+    env = build_ours(wl, batch, args.distinct_batches, rank, device, world=world, gather=gather)
+    ctx, batches, fetch = env["ctx"], env["batches"], env["fetch"]
     n_cand = sum(len(l["cand_idtok"]) for l in batches[0])
     out_bufs = {"logits": torch.empty((batch, wl.shape.vocab), dtype=torch.float32, device=device),
                 "cand_scores": torch.empty((n_cand,), dtype=torch.float32, device=device)}
     stream = torch.cuda.current_stream(device)
 
     def step(i, out=out_bufs):
-        lay = batches[i % len(batches)]
+        b = i % len(batches)
+        lay = batches[b]
+        if fetch is not None and fetch[b]:  # pull peer-resident candidate items over NVLink (§8(e))
+            f = fetch[b]
+            ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], [x[2] for x in f], [wl.item_len] * len(f),
+                             [wl.prefix_len] * len(f), stream=stream)
         seqs = ctx.assemble(lay, prefix_id=1, gather_from=c, stream=stream)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
                               out=out, stream=stream)
@@ -392,8 +441,9 @@ def run_ours(args, wl):
            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded generators, random-init weights)",
            "config": {"workload": wl.name, "batch": batch, "seq_len": wl.n, "r": r_bp / 1e4, "check_layer": c,
-                      "parallelism": f"dp{world} (independent request streams)",
-                      "l2": "inputs larger than L2 (16 GB weights, 34 GB item pool)"},
+                      "parallelism": (f"dp{world}: Alg. 1 sharded item pool, Eq. 2 routing, NVLink fetch"
+                                      if world > 1 else "dp1"),
+                      "l2": "inputs larger than L2 (16 GB weights + item pool per GPU)"},
            "ttft_ms": {"p50": float(np.percentile(step_ms, 50, method="inverted_cdf")),
                        "p99": float(np.percentile(step_ms, 99, method="inverted_cdf")),
                        "note": "batch mode: every request of a batch is submitted at the step start"},
@@ -404,6 +454,12 @@ def run_ours(args, wl):
            "kernels": kern, "gpu_launches": int(launches), "clocks": cl,
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_bytes(batches[0]),
                    "d2h_bytes_per_step": int(pin_l.numel() * 4 + pin_c.numel() * 4)}}
+    if env["shard"] is not None:
+        sh = env["shard"]
+        res["shard"] = {"k": world, "edge_cut": sh["cut"], "hot_replicated": int((sh["part"] == -1).sum()),
+                        "items_on_rank0": int(sh["res"][0].sum()), "routed_per_rank": sh["routed"],
+                        "rank0_local_hit": sh["local_hit"],
+                        "rank0_fetch_items_per_batch": sh.get("fetch_items_per_batch")}
     if world == 1 and not args.no_baselines and not args.profile_only:
         res["baselines"] = baselines(args, wl, env, r_bp, c, step_ms)
     if world == 1 and not args.no_cpu_baseline and not args.profile_only:
