@@ -22,8 +22,10 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
   __nv_bfloat16 h = __float2bfloat16_rn(f);
   return *reinterpret_cast<uint16_t*>(&h);
 }
+// two fp32 -> packed bf16x2 (low = a), one cvt.rn.bf16x2.f32 (RNE, same rounding as f2bf)
 __device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
-  return static_cast<uint32_t>(f2bf(a)) | (static_cast<uint32_t>(f2bf(b)) << 16);
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 // Eq. 3 divergence term in the SURVEY R4 fixed point: y = fp32(|a - b|) where a is the bf16

@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int t = r / G, g = r % G;
     const bool valid = (r < TQ * G) && (t < n_rows);
     const int p = valid ? a.qpos[row_start + t] : -1;
+    const int p_first = a.qpos[row_start];  // smallest position of the tile (rows sorted by position)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t sr[SCOLS];
@@ -167,14 +168,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_wait_ld();
       const int key0 = j * BKV + col0;
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
+      if (j * BKV + BKV - 1 <= p_first) {  // every row of the tile sees every key: no causal mask
 #pragma unroll
-      for (int c = 0; c < SCOLS; ++c) {
-        float v = __uint_as_float(sr[c]) * a.scale_log2;
-        v = (key0 + c <= p) ? v : -INFINITY;
-        sr[c] = __float_as_uint(v);
-        mx4[c & 3] = fmaxf(mx4[c & 3], v);
+        for (int c = 0; c < SCOLS; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sr[c]));
+      } else {
+#pragma unroll
+        for (int c = 0; c < SCOLS; ++c) {
+          const float v = (key0 + c <= p) ? __uint_as_float(sr[c]) : -INFINITY;
+          sr[c] = __float_as_uint(v);
+          mx4[c & 3] = fmaxf(mx4[c & 3], v);
+        }
       }
-      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      // scores stay raw; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
+      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
       // combine the two column halves of this row (warp pair q+4 / q+8, named barrier 1+q)
       red[(j & 1) * 256 + hf * 128 + r] = mx;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
@@ -209,7 +215,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int c = 0; c < SCOLS; c += 8) {
         float e[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) { e[i] = fast_exp2(__uint_as_float(sr[c + i]) - base); ls[i & 3] += e[i]; }
+        for (int i = 0; i < 8; ++i) {
+          e[i] = fast_exp2(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base));
+          ls[i & 3] += e[i];
+        }
         uint4 u;
         u.x = pack_bf2(e[0], e[1]); u.y = pack_bf2(e[2], e[3]); u.z = pack_bf2(e[4], e[5]); u.w = pack_bf2(e[6], e[7]);
         const int chunk = c >> 3;

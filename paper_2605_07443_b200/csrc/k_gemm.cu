@@ -138,7 +138,7 @@ __device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool ro
 
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, int M, int N, int lane_base,
-                                              const EpiArgs& ep) {
+                                              const EpiArgs& ep, bool atomic) {
   const int row = m0 + lane_base + (threadIdx.x & 31);
   const bool row_ok = row < M;
   if constexpr (EPI == EPI_BF16 || EPI == EPI_F32 || EPI == EPI_ADD_F32) {
@@ -154,6 +154,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
           const int64_t idx = static_cast<int64_t>(row) * ep.ldo + n0 + c + j;
           if constexpr (EPI == EPI_BF16) static_cast<uint16_t*>(ep.out)[idx] = f2bf(val);
           else if constexpr (EPI == EPI_F32) static_cast<float*>(ep.out)[idx] = val;
+          else if (atomic) atomicAdd(static_cast<float*>(ep.out) + idx, val);
           else static_cast<float*>(ep.out)[idx] += val;
         }
         continue;
@@ -167,6 +168,10 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
         for (int j = 0; j < 4; ++j) {
           float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           if constexpr (EPI == EPI_ADD_F32) {
+            if (atomic) {  // split-K partial sums meet in the fp32 residual stream
+              atomicAdd(o + j, w);
+              continue;
+            }
             const float4 x = o[j];
             w.x += x.x; w.y += x.y; w.z += x.z; w.w += x.w;
           }
@@ -199,7 +204,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
 template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-           const EpiArgs ep) {
+           int splits, const EpiArgs ep) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -227,13 +232,16 @@ __global__ void __launch_bounds__(256, 1)
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
+  // work unit u = (tile u / splits, K-split u % splits); splits > 1 only for additive epilogues
+  const int units = tiles * splits;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0; uint32_t phase = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        int mb, nb; tile_coords(t, num_m, num_n, mb, nb);
-        for (int kb = 0; kb < nk; ++kb) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int mb, nb; tile_coords(u / splits, num_m, num_n, mb, nb);
+        const int sp = u % splits;
+        for (int kb = sp * nk / splits; kb < (sp + 1) * nk / splits; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
@@ -246,20 +254,21 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {  // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
       int stage = 0; uint32_t phase = 0; int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        const int sp = u % splits, kb0 = sp * nk / splits;
+        for (int kb = kb0; kb < (sp + 1) * nk / splits; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -269,14 +278,14 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {  // ---------------- epilogue warps
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      int mb, nb; tile_coords(t, num_m, num_n, mb, nb);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+      int mb, nb; tile_coords(u / splits, num_m, num_n, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      epilogue_tile<BN, EPI>(taddr, mb * BM, nb * BN, M, N, q * 32, ep);
+      epilogue_tile<BN, EPI>(taddr, mb * BM, nb * BN, M, N, q * 32, ep, splits > 1);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -298,8 +307,22 @@ cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, int M, int N,
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  k_gemm<BN, EPI><<<grid, 256, C::SMEM, s>>>(*a, *b, M, N, K, ep);
+  const int nk = (K + BK - 1) / BK;
+  // split-K for additive epilogues when the tile count fills the SMs badly: pick the split that
+  // minimises waves * (k-blocks per unit + fixed per-unit overhead of ~6 k-blocks)
+  int splits = 1;
+  if (EPI == EPI_ADD_F32) {
+    auto cost = [&](int sp) {
+      const int64_t units = static_cast<int64_t>(tiles) * sp;
+      return ((units + num_sms - 1) / num_sms) * ((nk + sp - 1) / sp + 6);
+    };
+    int64_t best = cost(1);
+    for (int sp = 2; sp <= 16 && nk / sp >= 8; ++sp)
+      if (cost(sp) * 100 < best * 95) { best = cost(sp); splits = sp; }
+  }
+  const int units = tiles * splits;
+  const int grid = units < num_sms ? units : num_sms;
+  k_gemm<BN, EPI><<<grid, 256, C::SMEM, s>>>(*a, *b, M, N, K, splits, ep);
   return cudaGetLastError();
 }
 
