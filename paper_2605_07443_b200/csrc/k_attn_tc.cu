@@ -6,11 +6,13 @@
 //   warp 0 lane 0   TMA: Q once (3-D box [TQ][G][64] x 2 halves), K tiles (2-stage ring)
 //   warp 3 lane 0   TMA: V tiles (2-stage ring)
 //   warp 1 lane 0   MMA: S_j = Q K_j^T (M=128, N=128, K=128; A, B K-major SW128) into TMEM S[j%2];
-//                        O += P_j V_j (A = P from smem, K-major; B = V MN-major SW128) into TMEM O
-//   warps 4..7      softmax: thread = row; tcgen05.ld S row, causal mask by true position,
-//                   online max with lazy O rescale (only when the max grows by > 2^8, done on the
-//                   TMEM accumulator with tcgen05.ld/st), P = exp2(s - m) -> bf16 -> swizzled smem
-// Issue order S_0, S_1, PV_0, S_2, PV_1, ... so softmax of tile j+1 overlaps PV_j.
+//                        O += P_j V_j (A = P from TMEM, TS mode; B = V MN-major SW128) into TMEM O
+//   warps 4..     softmax, NSPLIT warps per TMEM lane quarter: thread = (row, SCOLS key columns);
+//                 tcgen05.ld its S slice, causal mask by true position (skipped on full tiles), row max
+//                 combined over the NSPLIT warps through smem + a named barrier, online max with lazy
+//                 O rescale (only when the max grows by > 2^8, on the TMEM accumulator with
+//                 tcgen05.ld/st), P = 2^(s*scale - m) -> bf16 pairs -> TMEM (over the S tile)
+// Issue order S_0, S_1, PV_0, S_2, PV_1, ... so softmax of tile j+1 overlaps PV_j and S_{j+2}.
 #include "common.cuh"
 #include "rc_internal.h"
 
@@ -20,11 +22,12 @@ namespace {
 constexpr int DH = 128, BKV = 128, ROWS = 128;
 constexpr uint32_t HALF = ROWS * 64 * 2;  // one [128 rows][64 bf16] SW128 sub-tile = 16 KB
 constexpr uint32_t TILE = 2 * HALF;       // 32 KB
-constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = 3 * TILE, OFF_P = 5 * TILE, OFF_BAR = 7 * TILE;
-constexpr uint32_t OFF_RED = OFF_BAR + 256;            // [2 tile slots][2 column halves][128 rows] f32
-constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
-constexpr int SCOLS = BKV / 2;                          // S columns per softmax thread (two warps per row)
-constexpr int NTHREADS = 384;                           // 4 control warps + 8 softmax warps
+constexpr int NSPLIT = 2;                               // softmax warps per TMEM lane quarter (column split)
+constexpr int SCOLS = BKV / NSPLIT;                     // S columns per softmax thread
+constexpr int NTHREADS = 128 + 128 * NSPLIT;            // 4 control warps + 4*NSPLIT softmax warps
+constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = 3 * TILE, OFF_BAR = 5 * TILE;
+constexpr uint32_t OFF_RED = OFF_BAR + 256;            // [2 tile slots][NSPLIT][128 rows] f32
+constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * NSPLIT * 128 * 4;
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -33,11 +36,23 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA/ALU pipes: x = n + f (n = round(x) via the 1.5*2^23 magic constant, |f| <= 1/2),
+// 2^f by a degree-3 Taylor polynomial (relative error < 7e-4, below the bf16 rounding of P), then
+// n added into the exponent field. Inputs below -127 underflow to ~0.
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.0555041086648216f, 0.2402265069591007f);
+  p = fmaf(p, f, 0.6931471805599453f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int64_t t_cap) {
-  // 224 KB of tiles + barriers + exchange: no room for a manual 1 KB alignment pad, so the
-  // dynamic window must itself be 1024-aligned (SWIZZLE_128B atoms); checked below.
+  // SWIZZLE_128B atoms need a 1024-aligned dynamic window; checked below.
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -45,7 +60,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   float* red = reinterpret_cast<float*>(smem + OFF_RED);
   uint8_t* sK = smem + OFF_K;
   uint8_t* sV = smem + OFF_V;
-  uint8_t* sP = smem + OFF_P;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;   // [2]
@@ -72,7 +86,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&pv_done[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 32 * 4 * NSPLIT); mbar_init(&pv_done[i], 1);
     }
     fence_barrier_init();
     fence_proxy_async();
@@ -137,10 +151,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(&v_full[b], (j >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(smem_u32(sP + b * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
+        for (int k = 0; k < BKV / 16; ++k) {  // A = P_j from TMEM (8 columns per 16 keys), B = V MN-major
           const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + b * TILE + k * 2048), HALF, 1024);
-          umma_bf16(tmem + 256, ad, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + 256, tmem + b * 128 + k * 8, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&v_empty[b]);
         umma_commit(&pv_done[b]);
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp >= 4) {  // ---- softmax: thread <-> (row, half of the key columns)
     const int q = warp & 3;              // TMEM lane quarter of this warp
-    const int hf = (warp - 4) >> 2;      // warps 4..7: keys 0..63 of a tile, warps 8..11: keys 64..127
+    const int hf = (warp - 4) >> 2;      // column split: keys [hf*SCOLS, (hf+1)*SCOLS) of every tile
     const int col0 = hf * SCOLS;
     const int r = q * 32 + lane;
     const int t = r / G, g = r % G;
@@ -182,9 +195,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // scores stay raw; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
       float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
       // combine the two column halves of this row (warp pair q+4 / q+8, named barrier 1+q)
-      red[(j & 1) * 256 + hf * 128 + r] = mx;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-      mx = fmaxf(mx, red[(j & 1) * 256 + (hf ^ 1) * 128 + r]);
+      float* rslot = red + (j & 1) * (NSPLIT * 128);
+      rslot[hf * 128 + r] = mx;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NSPLIT) : "memory");
+#pragma unroll
+      for (int o = 0; o < NSPLIT; ++o) mx = fmaxf(mx, rslot[o * 128 + r]);
       float alpha = 1.f;
       bool need = false;
       if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
@@ -208,32 +223,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       l_run *= alpha;
       const float base = (m_run == -INFINITY) ? 0.f : m_run;
-      if (j >= 2) mbar_wait(&pv_done[b], ((j - 2) >> 1) & 1);  // P buffer b free (PV_{j-2} done)
-      uint8_t* prow = sP + b * TILE + hf * HALF + r * 128;     // this half = one 64-key K-block of P
+      // P (bf16 pairs) overwrites the first 64 columns of this tile's S buffer in TMEM: every split has
+      // already loaded its S slice (the max exchange above is a barrier), and S_{j+2}, the next writer
+      // of the buffer, is issued after PV_j in the in-order tcgen05 stream.
       float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[SCOLS / 2];
 #pragma unroll
       for (int c = 0; c < SCOLS; c += 8) {
         float e[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          e[i] = fast_exp2(fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base));
+          const float x = fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base);
+          // one chunk in four on the FMA pipe: the SFU (16 ex2/clk/SM) is otherwise the co-bottleneck
+          e[i] = ((c >> 3) % 4 == 3) ? poly_exp2(x) : fast_exp2(x);
           ls[i & 3] += e[i];
         }
-        uint4 u;
-        u.x = pack_bf2(e[0], e[1]); u.y = pack_bf2(e[2], e[3]); u.z = pack_bf2(e[4], e[5]); u.w = pack_bf2(e[6], e[7]);
-        const int chunk = c >> 3;
-        *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) = u;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf2(e[2 * i], e[2 * i + 1]);
       }
       l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      fence_async_smem();
+#pragma unroll
+      for (int c = 0; c < SCOLS / 2; c += 32) tmem_st32(tmem + lane_base + b * 128 + col0 / 2 + c, pk + c);
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
     // epilogue: O / l -> bf16 (l = sum of the two halves' partial sums)
     // slot (nkv & 1) was last read before the final tile's barrier by both warps of the pair
-    red[(nkv & 1) * 256 + hf * 128 + r] = l_run;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
-    const float l_tot = l_run + red[(nkv & 1) * 256 + (hf ^ 1) * 128 + r];
+    float* lslot = red + (nkv & 1) * (NSPLIT * 128);
+    lslot[hf * 128 + r] = l_run;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NSPLIT) : "memory");
+    float l_tot = 0.f;
+#pragma unroll
+    for (int o = 0; o < NSPLIT; ++o) l_tot += lslot[o * 128 + r];
     mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
