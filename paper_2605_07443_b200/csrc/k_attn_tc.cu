@@ -6,13 +6,17 @@
 //   warp 0 lane 0   TMA: Q once (3-D box [TQ][G][64] x 2 halves), K tiles (2-stage ring)
 //   warp 3 lane 0   TMA: V tiles (2-stage ring)
 //   warp 1 lane 0   MMA: S_j = Q K_j^T (M=128, N=128, K=128; A, B K-major SW128) into TMEM S[j%2];
-//                        O += P_j V_j (A = P from TMEM, TS mode; B = V MN-major SW128) into TMEM O
-//   warps 4..     softmax, NSPLIT warps per TMEM lane quarter: thread = (row, SCOLS key columns);
-//                 tcgen05.ld its S slice, causal mask by true position (skipped on full tiles), row max
-//                 combined over the NSPLIT warps through smem + a named barrier, online max with lazy
-//                 O rescale (only when the max grows by > 2^8, on the TMEM accumulator with
-//                 tcgen05.ld/st), P = 2^(s*scale - m) -> bf16 pairs -> TMEM (over the S tile)
-// Issue order S_0, S_1, PV_0, S_2, PV_1, ... so softmax of tile j+1 overlaps PV_j and S_{j+2}.
+//                        O_h += P_{j,h} V_{j,h} for the two 64-key halves h of the tile (A = P from
+//                        TMEM, TS mode; B = V rows of that half, MN-major SW128) into TMEM O_h
+//   warps 4..11     softmax: two independent groups (key half h = 0, 1) of 4 warps; thread = (row,
+//                   64 keys of every tile). Each group keeps its own running max / sum and its own
+//                   accumulator O_h, so the groups never synchronise inside the KV loop and the MMA
+//                   warp can start PV on one half while the other is still in exp; the two partial
+//                   softmaxes are merged once at the end (flash-decoding style combine).
+//                   Per tile: tcgen05.ld of its S slice, causal mask by true position (skipped on
+//                   full tiles), lazy O_h rescale (only when the max grows by > 2^8),
+//                   P = 2^(s*scale - m) -> bf16 pairs -> TMEM over its own S columns.
+// TMEM: S[2] (2 x 128 columns) + O_0, O_1 (2 x 128) = 512 columns.
 #include "common.cuh"
 #include "rc_internal.h"
 
@@ -22,12 +26,13 @@ namespace {
 constexpr int DH = 128, BKV = 128, ROWS = 128;
 constexpr uint32_t HALF = ROWS * 64 * 2;  // one [128 rows][64 bf16] SW128 sub-tile = 16 KB
 constexpr uint32_t TILE = 2 * HALF;       // 32 KB
-constexpr int NSPLIT = 2;                               // softmax warps per TMEM lane quarter (column split)
-constexpr int SCOLS = BKV / NSPLIT;                     // S columns per softmax thread
-constexpr int NTHREADS = 128 + 128 * NSPLIT;            // 4 control warps + 4*NSPLIT softmax warps
-constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = 3 * TILE, OFF_BAR = 5 * TILE;
-constexpr uint32_t OFF_RED = OFF_BAR + 256;            // [2 tile slots][NSPLIT][128 rows] f32
-constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * NSPLIT * 128 * 4;
+constexpr int SCOLS = 64;                  // keys per softmax thread per tile (two key halves)
+constexpr int NTHREADS = 128 + 256;        // 4 control warps + 2 x 4 softmax warps
+constexpr int KST = 2, VST = 2;
+constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
+constexpr uint32_t OFF_RED = OFF_BAR + 256;  // [2 halves][2 (m, l)][128 rows] f32 for the final merge
+constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
+constexpr uint32_t O_COL = 256;            // O_h at 256 + 128 h
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -37,7 +42,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
 }
 
 // 2^x on the FMA/ALU pipes: x = n + f (n = round(x) via the 1.5*2^23 magic constant, |f| <= 1/2),
-// 2^f by a degree-3 Taylor polynomial (relative error < 7e-4, below the bf16 rounding of P), then
+// 2^f by a degree-3 Taylor polynomial (relative error < 8e-4, below the bf16 rounding of P), then
 // n added into the exponent field. Inputs below -127 underflow to ~0.
 __device__ __forceinline__ float poly_exp2(float x) {
   x = fmaxf(x, -127.f);
@@ -57,19 +62,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* smem = smem_raw;
   if ((smem_u32(smem) & 1023u) != 0) __trap();
   uint8_t* sQ = smem + OFF_Q;
-  float* red = reinterpret_cast<float*>(smem + OFF_RED);
   uint8_t* sK = smem + OFF_K;
   uint8_t* sV = smem + OFF_V;
+  float* red = reinterpret_cast<float*>(smem + OFF_RED);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;
-  uint64_t* v_empty = bars + 7;
-  uint64_t* s_full = bars + 9;
-  uint64_t* p_full = bars + 11;
-  uint64_t* pv_done = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* q_full = bars;                 // [1]
+  uint64_t* k_full = bars + 1;             // [KST]
+  uint64_t* k_empty = k_full + KST;        // [KST]
+  uint64_t* v_full = k_empty + KST;        // [VST]
+  uint64_t* v_empty = v_full + VST;        // [VST]
+  uint64_t* s_full = v_empty + VST;        // [2]
+  uint64_t* p_full = s_full + 2;           // [2 S buffers][2 halves]
+  uint64_t* pv_done = p_full + 4;          // [2 halves][2] alternating per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 4);
 
   const int4 tile = a.tiles[blockIdx.x];
   const int row_start = tile.x, n_rows = tile.y, kv_base = tile.z;
@@ -83,11 +88,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 32 * 4 * NSPLIT); mbar_init(&pv_done[i], 1);
-    }
+    for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 4; ++i) { mbar_init(&p_full[i], 128); mbar_init(&pv_done[i], 1); }
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -95,7 +99,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S0 at +0, S1 at +128, O at +256
+  const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- Q + K producer
@@ -105,11 +109,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tma_load_3d(sQ + HALF, &tmQ, q_full, 64, kvh * G, row_start);
       const int krow0 = static_cast<int>(kvh * t_cap + kv_base);
       for (int j = 0; j < nkv; ++j) {
-        const int b = j & 1;
-        mbar_wait(&k_empty[b], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&k_full[b], TILE);
-        tma_load_2d(sK + b * TILE, &tmK, &k_full[b], 0, krow0 + j * BKV);
-        tma_load_2d(sK + b * TILE + HALF, &tmK, &k_full[b], 64, krow0 + j * BKV);
+        const int s = j % KST;
+        mbar_wait(&k_empty[s], ((j / KST) & 1) ^ 1);
+        mbar_expect_tx(&k_full[s], TILE);
+        tma_load_2d(sK + s * TILE, &tmK, &k_full[s], 0, krow0 + j * BKV);
+        tma_load_2d(sK + s * TILE + HALF, &tmK, &k_full[s], 64, krow0 + j * BKV);
       }
     }
   } else if (warp == 3) {
@@ -117,11 +121,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tma_prefetch_desc(&tmV);
       const int vrow0 = static_cast<int>(kvh * t_cap + kv_base);
       for (int j = 0; j < nkv; ++j) {
-        const int b = j & 1;
-        mbar_wait(&v_empty[b], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&v_full[b], TILE);
-        tma_load_2d(sV + b * TILE, &tmV, &v_full[b], 0, vrow0 + j * BKV);
-        tma_load_2d(sV + b * TILE + HALF, &tmV, &v_full[b], 64, vrow0 + j * BKV);
+        const int s = j % VST;
+        mbar_wait(&v_empty[s], ((j / VST) & 1) ^ 1);
+        mbar_expect_tx(&v_full[s], TILE);
+        tma_load_2d(sV + s * TILE, &tmV, &v_full[s], 0, vrow0 + j * BKV);
+        tma_load_2d(sV + s * TILE + HALF, &tmV, &v_full[s], 64, vrow0 + j * BKV);
       }
     }
   } else if (warp == 1) {
@@ -130,54 +134,58 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t idPV = idesc_bf16_f32_bmn(128, 128);
       mbar_wait(q_full, 0);
       tc_fence_after();
-      auto issue_s = [&](int j) {
-        const int b = j & 1;
-        mbar_wait(&k_full[b], (j >> 1) & 1);
+      auto issue_s = [&](int j) {  // S_j into buffer j % 2
+        const int s = j % KST;
+        mbar_wait(&k_full[s], (j / KST) & 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const uint64_t ad = sdesc_sw128(smem_u32(sQ + (k >> 2) * HALF)) + 2 * (k & 3);
-          const uint64_t bd = sdesc_sw128(smem_u32(sK + b * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
-          umma_bf16(tmem + b * 128, ad, bd, idS, k > 0);
+          const uint64_t bd = sdesc_sw128(smem_u32(sK + s * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
+          umma_bf16(tmem + (j & 1) * 128, ad, bd, idS, k > 0);
         }
-        umma_commit(&k_empty[b]);
-        umma_commit(&s_full[b]);
+        umma_commit(&k_empty[s]);
+        umma_commit(&s_full[j & 1]);
       };
       issue_s(0);
       if (nkv > 1) issue_s(1);
       for (int j = 0; j < nkv; ++j) {
-        const int b = j & 1;
-        mbar_wait(&p_full[b], (j >> 1) & 1);
-        mbar_wait(&v_full[b], (j >> 1) & 1);
-        tc_fence_after();
+        const int b = j & 1, v = j % VST;
+        mbar_wait(&v_full[v], (j / VST) & 1);
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&p_full[b * 2 + h], (j >> 1) & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {  // A = P_j from TMEM (8 columns per 16 keys), B = V MN-major
-          const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + b * TILE + k * 2048), HALF, 1024);
-          umma_bf16_ts(tmem + 256, tmem + b * 128 + k * 8, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < 4; ++k) {  // 64 keys: A = P_{j,h} (8 TMEM columns per 16 keys), B = V rows
+            const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + v * TILE + (4 * h + k) * 2048), HALF, 1024);
+            umma_bf16_ts(tmem + O_COL + h * 128, tmem + b * 128 + h * 64 + k * 8, bd, idPV,
+                         (j > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&pv_done[h * 2 + (j & 1)]);
         }
-        umma_commit(&v_empty[b]);
-        umma_commit(&pv_done[b]);
-        if (j + 2 < nkv) issue_s(j + 2);
+        umma_commit(&v_empty[v]);
+        if (j + 2 < nkv) issue_s(j + 2);  // buffer b: both halves' P_j consumed by the PVs just issued
       }
     }
-  } else if (warp >= 4) {  // ---- softmax: thread <-> (row, half of the key columns)
+  } else if (warp >= 4) {  // ---- softmax: group h = key half, thread <-> (row, 64 keys of each tile)
     const int q = warp & 3;              // TMEM lane quarter of this warp
-    const int hf = (warp - 4) >> 2;      // column split: keys [hf*SCOLS, (hf+1)*SCOLS) of every tile
-    const int col0 = hf * SCOLS;
+    const int h = (warp - 4) >> 2;       // key half
+    const int col0 = h * SCOLS;
     const int r = q * 32 + lane;
     const int t = r / G, g = r % G;
     const bool valid = (r < TQ * G) && (t < n_rows);
     const int p = valid ? a.qpos[row_start + t] : -1;
     const int p_first = a.qpos[row_start];  // smallest position of the tile (rows sorted by position)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t o_col = O_COL + h * 128;
     float m_run = -INFINITY, l_run = 0.f;
     uint32_t sr[SCOLS];
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < SCOLS; c += 32) tmem_ld32(tmem + lane_base + b * 128 + col0 + c, sr + c);
+      tmem_ld32(tmem + lane_base + b * 128 + col0, sr);
+      tmem_ld32(tmem + lane_base + b * 128 + col0 + 32, sr + 32);
       tmem_wait_ld();
       const int key0 = j * BKV + col0;
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
@@ -193,13 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       // scores stay raw; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
-      float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
-      // combine the two column halves of this row (warp pair q+4 / q+8, named barrier 1+q)
-      float* rslot = red + (j & 1) * (NSPLIT * 128);
-      rslot[hf * 128 + r] = mx;
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NSPLIT) : "memory");
-#pragma unroll
-      for (int o = 0; o < NSPLIT; ++o) mx = fmaxf(mx, rslot[o * 128 + r]);
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
       float alpha = 1.f;
       bool need = false;
       if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
@@ -207,25 +209,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (m_run != -INFINITY) { alpha = fast_exp2(m_run - m_new); need = true; }
         m_run = m_new;
       }
-      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this warp's half of the TMEM accumulator rows
-        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this group's accumulator rows (rare)
+        mbar_wait(&pv_done[h * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
         tc_fence_after();
         uint32_t o[32];
 #pragma unroll
-        for (int c = 0; c < SCOLS; c += 32) {
-          tmem_ld32(tmem + lane_base + 256 + col0 + c, o);
+        for (int c = 0; c < DH; c += 32) {
+          tmem_ld32(tmem + lane_base + o_col + c, o);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(tmem + lane_base + 256 + col0 + c, o);
+          tmem_st32(tmem + lane_base + o_col + c, o);
         }
         tmem_wait_st();
       }
       l_run *= alpha;
       const float base = (m_run == -INFINITY) ? 0.f : m_run;
-      // P (bf16 pairs) overwrites the first 64 columns of this tile's S buffer in TMEM: every split has
-      // already loaded its S slice (the max exchange above is a barrier), and S_{j+2}, the next writer
-      // of the buffer, is issued after PV_j in the in-order tcgen05 stream.
+      // P (bf16 pairs) overwrites the first 32 of this group's own 64 S columns (already in registers)
       float ls[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[SCOLS / 2];
 #pragma unroll
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float x = fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base);
-          // one chunk in four on the FMA pipe: the SFU (16 ex2/clk/SM) is otherwise the co-bottleneck
+          // one chunk in four on the FMA pipe: the SFU (16 ex2/clk/SM) is the co-bottleneck
           e[i] = ((c >> 3) % 4 == 3) ? poly_exp2(x) : fast_exp2(x);
           ls[i & 3] += e[i];
         }
@@ -242,37 +242,42 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf2(e[2 * i], e[2 * i + 1]);
       }
       l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-#pragma unroll
-      for (int c = 0; c < SCOLS / 2; c += 32) tmem_st32(tmem + lane_base + b * 128 + col0 / 2 + c, pk + c);
+      tmem_st32(tmem + lane_base + b * 128 + col0, pk);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[b]);
+      mbar_arrive(&p_full[b * 2 + h]);
     }
-    // epilogue: O / l -> bf16 (l = sum of the two halves' partial sums)
-    // slot (nkv & 1) was last read before the final tile's barrier by both warps of the pair
-    float* lslot = red + (nkv & 1) * (NSPLIT * 128);
-    lslot[hf * 128 + r] = l_run;
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(32 * NSPLIT) : "memory");
-    float l_tot = 0.f;
-#pragma unroll
-    for (int o = 0; o < NSPLIT; ++o) l_tot += lslot[o * 128 + r];
-    mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
-    tc_fence_after();
+    // merge the two halves: O = (O_0 2^(m_0-m) + O_1 2^(m_1-m)) / (l_0 2^(m_0-m) + l_1 2^(m_1-m))
+    red[(h * 2 + 0) * 128 + r] = m_run;
+    red[(h * 2 + 1) * 128 + r] = l_run;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+    const float m0 = red[0 * 128 + r], l0 = red[1 * 128 + r], m1 = red[2 * 128 + r], l1 = red[3 * 128 + r];
+    const float m = fmaxf(m0, m1);
+    const float mb = (m == -INFINITY) ? 0.f : m;
+    const float f0 = (m0 == -INFINITY) ? 0.f : fast_exp2(m0 - mb);
+    const float f1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mb);
+    const float l_tot = l0 * f0 + l1 * f1;
     const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-    uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + col0;
+    const float w0 = f0 * inv, w1 = f1 * inv;
+    mbar_wait(&pv_done[0 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
+    mbar_wait(&pv_done[1 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
+    tc_fence_after();
+    // this thread writes output columns [h*64, h*64 + 64) of its row
+    uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + h * 64;
 #pragma unroll
-    for (int c = 0; c < SCOLS; c += 32) {
-      uint32_t o[32];
-      tmem_ld32(tmem + lane_base + 256 + col0 + c, o);
+    for (int c = 0; c < 64; c += 32) {
+      uint32_t o0[32], o1[32];
+      tmem_ld32(tmem + lane_base + O_COL + h * 64 + c, o0);
+      tmem_ld32(tmem + lane_base + O_COL + 128 + h * 64 + c, o1);
       tmem_wait_ld();
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
+          float y[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) y[k] = __uint_as_float(o0[i + k]) * w0 + __uint_as_float(o1[i + k]) * w1;
           uint4 u;
-          u.x = pack_bf2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-          u.y = pack_bf2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          u.z = pack_bf2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-          u.w = pack_bf2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+          u.x = pack_bf2(y[0], y[1]); u.y = pack_bf2(y[2], y[3]); u.z = pack_bf2(y[4], y[5]); u.w = pack_bf2(y[6], y[7]);
           *reinterpret_cast<uint4*>(dst + c + i) = u;
         }
       }

@@ -25,9 +25,61 @@ struct GemmCfg {
   static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
-  static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+  // residual epilogue staging: per epilogue warp 2 x [32 rows][32 fp32] SW128 boxes (TMA reduce-add)
+  static constexpr uint32_t STAGE_OUT = 4 * 2 * 32 * 32 * 4;
+  static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + STAGE_OUT + 1024 + 256;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
+
+__device__ __forceinline__ void tma_reduce_add_2d(const void* map, const void* smem_src, int c0, int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Residual epilogue: x[rows][cols] += acc through TMA reduce-add (fp32, atomic per element, so split-K
+// partial tiles simply add up). Each epilogue warp owns its 32 accumulator rows: tcgen05.ld 32 columns,
+// write them as one swizzled [32][32] box to its staging buffer, and let one lane issue the bulk
+// reduction; two buffers per warp keep a store in flight while the next chunk is loaded.
+template <int BN>
+__device__ __forceinline__ void epilogue_add_tma(uint32_t taddr, int m0, int n0, int N, int q, const void* tmC,
+                                                 uint8_t* stage, int& chunk_ctr) {
+  const int lane = threadIdx.x & 31;
+  uint8_t* mybuf = stage + q * 2 * 4096;
+  for (int c = 0; c < BN; c += 32) {
+    if (n0 + c >= N) break;
+    const int buf = chunk_ctr & 1;
+    if (chunk_ctr >= 2) {
+      if (lane == 0) bulk_wait_read<1>();  // the reduction that last read this buffer has drained it
+      __syncwarp();
+    }
+    uint32_t v[32];
+    tmem_ld32(taddr + c, v);
+    tmem_wait_ld();
+    uint8_t* row = mybuf + buf * 4096 + lane * 128;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      *reinterpret_cast<uint4*>(row + ((k ^ (lane & 7)) << 4)) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_reduce_add_2d(tmC, mybuf + buf * 4096, n0 + c, m0 + q * 32);
+      bulk_commit();
+    }
+    ++chunk_ctr;
+  }
+}
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
   const int per_group = GROUP_M * num_n;
@@ -203,14 +255,15 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-           int splits, const EpiArgs ep) {
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits, const EpiArgs ep) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+  uint8_t* sOut = sB + C::STAGES * C::B_BYTES;  // 1024-aligned: A/B stage sizes are multiples of 16 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + C::STAGE_OUT);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -277,7 +330,8 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue warps
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-    int it = 0;
+    int it = 0, chunk_ctr = 0;
+    if (EPI == EPI_ADD_F32 && (threadIdx.x & 31) == 0) tma_prefetch_desc(&tmC);
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
       int mb, nb; tile_coords(u / splits, num_m, num_n, mb, nb);
       const int acc = it & 1;
@@ -285,9 +339,14 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      epilogue_tile<BN, EPI>(taddr, mb * BM, nb * BN, M, N, q * 32, ep, splits > 1);
+      if constexpr (EPI == EPI_ADD_F32) epilogue_add_tma<BN>(taddr, mb * BM, nb * BN, N, q, &tmC, sOut, chunk_ctr);
+      else epilogue_tile<BN, EPI>(taddr, mb * BM, nb * BN, M, N, q * 32, ep, splits > 1);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+    }
+    if constexpr (EPI == EPI_ADD_F32) {
+      if ((threadIdx.x & 31) == 0) bulk_wait<0>();  // reductions complete before the CTA retires
+      __syncwarp();
     }
   }
   tc_fence_before();
@@ -297,8 +356,9 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 template <int BN, int EPI>
-cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, int M, int N, int K, const EpiArgs& ep, int num_sms,
-                       cudaStream_t s) {
+cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K,
+                       const EpiArgs& ep, int num_sms, cudaStream_t s) {
+  if (EPI == EPI_ADD_F32 && c == nullptr) return cudaErrorInvalidValue;
   using C = GemmCfg<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -322,7 +382,7 @@ cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, int M, int N,
   }
   const int units = tiles * splits;
   const int grid = units < num_sms ? units : num_sms;
-  k_gemm<BN, EPI><<<grid, 256, C::SMEM, s>>>(*a, *b, M, N, K, splits, ep);
+  k_gemm<BN, EPI><<<grid, 256, C::SMEM, s>>>(*a, *b, c ? *c : *a, M, N, K, splits, ep);
   return cudaGetLastError();
 }
 
@@ -373,11 +433,24 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
-cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, int M, int N, int K, int bn, int epi,
-                        const EpiArgs& ep, int num_sms, cudaStream_t s) {
+bool make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K, int bn,
+                        int epi, const EpiArgs& ep, int num_sms, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;
 #define RC_GEMM_CASE(BN_, E_) \
-  if (bn == BN_ && epi == E_) return launch_one<BN_, E_>(a, b, M, N, K, ep, num_sms, s);
+  if (bn == BN_ && epi == E_) return launch_one<BN_, E_>(a, b, c, M, N, K, ep, num_sms, s);
   RC_GEMM_CASE(256, EPI_BF16) RC_GEMM_CASE(256, EPI_F32) RC_GEMM_CASE(256, EPI_ADD_F32)
   RC_GEMM_CASE(256, EPI_SWIGLU) RC_GEMM_CASE(256, EPI_QKV) RC_GEMM_CASE(256, EPI_DEV)
   RC_GEMM_CASE(128, EPI_BF16) RC_GEMM_CASE(128, EPI_F32) RC_GEMM_CASE(128, EPI_ADD_F32)

@@ -204,6 +204,7 @@ struct rc_ctx {
   int32_t* sel_urow = nullptr;
   // tensor maps
   CUtensorMap mA_a{}, mA_o{}, mA_h{};
+  CUtensorMap mC_x{}, mC_xs{};  // fp32 residual streams as TMA reduce-add targets
   std::vector<CUtensorMap> mB_qkv, mB_kv, mB_o, mB_gu, mB_d;
   CUtensorMap mB_lm{};
   bool attn_tc = false;                 // tcgen05 attention (head_dim 128)
@@ -396,10 +397,18 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   c->sel_pos = dev_alloc<int32_t>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace sel");
   c->sel_dst = dev_alloc<int32_t>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace sel");
   c->sel_urow = dev_alloc<int32_t>(Mx, &e); if (e) return fail(RC_E_NOMEM, "workspace sel");
+  // finite contents everywhere: GEMM tiles read stale rows past M (never stored, but reduce-added
+  // into unused residual rows), which must not hold NaN bit patterns
+  RC_CUDA(cudaMemset(c->x, 0, Mx * d * 4));
+  RC_CUDA(cudaMemset(c->xs, 0, Mx * d * 4));
+  RC_CUDA(cudaMemset(c->a, 0, Mx * d * 2));
+  RC_CUDA(cudaMemset(c->o, 0, Mx * H * dh * 2));
+  RC_CUDA(cudaMemset(c->h, 0, Mx * F * 2));
   // tensor maps: A operands (rows = Mx; tiles never read beyond the call's M-tile), B = weights
   bool ok = make_tmap_bf16_2d(&c->mA_a, c->a, Mx, d, d, 128) &&
             make_tmap_bf16_2d(&c->mA_o, c->o, Mx, H * dh, H * dh, 128) &&
-            make_tmap_bf16_2d(&c->mA_h, c->h, Mx, F, F, 128);
+            make_tmap_bf16_2d(&c->mA_h, c->h, Mx, F, F, 128) && make_tmap_f32_2d(&c->mC_x, c->x, Mx, d, d) &&
+            make_tmap_f32_2d(&c->mC_xs, c->xs, Mx, d, d);
   c->bn_qkv = pick_bn(c->Nqkv);
   c->bn_kv = pick_bn(2 * Hk * dh);
   c->bn_o = pick_bn(d);
@@ -755,8 +764,9 @@ rc_status rc_sel_count(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_pr
 
 namespace {
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
-rc_status run_layer(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_pos, const int32_t* d_dst,
-                    const int4* d_tiles, int32_t n_tiles, double attn_flops, int attn_pending, cudaStream_t s) {
+rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
+                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, double attn_flops, int attn_pending,
+                    cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
   const double R = rows, norm_b = R * d * 6.0;
@@ -770,7 +780,7 @@ rc_status run_layer(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_p
   ep.rope_cos = c->rope_cos; ep.rope_sin = c->rope_sin; ep.rope_zero = c->rope_zero;
   ep.n_heads = H; ep.n_kv_heads = Hk; ep.head_dim = dh;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, c->Nqkv, d), gemm_bytes(R, c->Nqkv, d, 2), -1,
-            gemm_launch(&c->mA_a, &c->mB_qkv[l], rows, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s));
+            gemm_launch(&c->mA_a, &c->mB_qkv[l], nullptr, rows, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s));
   AttnArgs at{};
   at.q = c->q; at.o = c->o; at.qpos = d_pos; at.tiles = d_tiles; at.n_tiles = n_tiles;
   at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
@@ -784,16 +794,16 @@ rc_status run_layer(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_p
   EpiArgs eo{};
   eo.out = x; eo.ldo = d;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, H * dh), gemm_bytes(R, d, H * dh, 8), -1,
-            gemm_launch(&c->mA_o, &c->mB_o[l], rows, d, H * dh, c->bn_o, EPI_ADD_F32, eo, c->num_sms, s));
+            gemm_launch(&c->mA_o, &c->mB_o[l], mx, rows, d, H * dh, c->bn_o, EPI_ADD_F32, eo, c->num_sms, s));
   RC_LAUNCH(RC_K_SMALL, 0, norm_b, -1, rmsnorm_launch(x, nullptr, rows, d, c->ln2[l], m.rms_eps, c->a, s));
   EpiArgs eg{};
   eg.out = c->h; eg.ldo = F;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, 2.0 * F, d), gemm_bytes(R, 2.0 * F, d, 1), -1,
-            gemm_launch(&c->mA_a, &c->mB_gu[l], rows, 2 * F, d, 256, EPI_SWIGLU, eg, c->num_sms, s));
+            gemm_launch(&c->mA_a, &c->mB_gu[l], nullptr, rows, 2 * F, d, 256, EPI_SWIGLU, eg, c->num_sms, s));
   EpiArgs ed{};
   ed.out = x; ed.ldo = d;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, F), gemm_bytes(R, d, F, 8), -1,
-            gemm_launch(&c->mA_h, &c->mB_d[l], rows, d, F, c->bn_d, EPI_ADD_F32, ed, c->num_sms, s));
+            gemm_launch(&c->mA_h, &c->mB_d[l], mx, rows, d, F, c->bn_d, EPI_ADD_F32, ed, c->num_sms, s));
   return RC_OK;
 }
 }  // namespace
@@ -891,7 +901,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   attn_u *= 4.0 * m.n_heads * m.head_dim;
   const int pend_idx = c->prof ? static_cast<int>(c->pend.size()) : -1;
   for (int l = 0; l < cL; ++l) {
-    st = run_layer(c, l, c->x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, attn_u, -1, s);
+    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, attn_u, -1, s);
     if (st != RC_OK) return st;
   }
   // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
@@ -909,7 +919,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     ev.dev_out = c->dev; ev.row_reuse = reinterpret_cast<const uint8_t*>(db + o_reuse);
     const double Nkv = 2.0 * m.n_kv_heads * m.head_dim;
     RC_LAUNCH(RC_K_GEMM, gemm_flops(U, Nkv, d), gemm_bytes(U, Nkv, d, 2), -1,
-              gemm_launch(&c->mA_a, &c->mB_kv[cL], U, 2 * m.n_kv_heads * m.head_dim, d, c->bn_kv, EPI_DEV, ev,
+              gemm_launch(&c->mA_a, &c->mB_kv[cL], nullptr, U, 2 * m.n_kv_heads * m.head_dim, d, c->bn_kv, EPI_DEV, ev,
                           c->num_sms, s));
     // ---- a4: selection
     SelectArgs sa{};
@@ -927,7 +937,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
             gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
   // ---- a5-a7: selective layers c..L-1 on Sel
   for (int l = cL; l < L; ++l) {
-    st = run_layer(c, l, c->xs, S, c->sel_pos, c->sel_dst, d_st, n_st, 0.0, pend_idx, s);
+    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, 0.0, pend_idx, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout
@@ -946,7 +956,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   EpiArgs el{};
   el.out = lg; el.ldo = m.vocab;
   RC_LAUNCH(RC_K_LMHEAD, gemm_flops(n_req, m.vocab, d), gemm_bytes(n_req, m.vocab, d, 4), -1,
-            gemm_launch(&c->mA_a, &c->mB_lm, n_req, m.vocab, d, c->bn_lm, EPI_F32, el, c->num_sms, s));
+            gemm_launch(&c->mA_a, &c->mB_lm, nullptr, n_req, m.vocab, d, c->bn_lm, EPI_F32, el, c->num_sms, s));
   if (cand_scores && n_cand > 0)
     RC_LAUNCH(RC_K_SMALL, 0, n_cand * 12.0, -1,
               cand_scores_launch(lg, m.vocab, D32(o_creq), D32(o_cid), n_cand, cand_scores, s));
@@ -1108,7 +1118,7 @@ rc_status rc_diag_gemm(int32_t M, int32_t N, int32_t K, const void* A, const voi
   RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   EpiArgs ep{};
   ep.out = C; ep.ldo = N;
-  RC_CUDA(gemm_launch(&ma, &mb, M, N, K, bn, EPI_F32, ep, sms, static_cast<cudaStream_t>(stream)));
+  RC_CUDA(gemm_launch(&ma, &mb, nullptr, M, N, K, bn, EPI_F32, ep, sms, static_cast<cudaStream_t>(stream)));
   return RC_OK;
 }
 

@@ -42,8 +42,10 @@ struct EpiArgs {
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
                        uint32_t box_rows);
-cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, int M, int N, int K, int bn, int epi,
-                        const EpiArgs& ep, int num_sms, cudaStream_t s);
+// c: output tensor map (fp32 [rows][cols], 32x32 SW128 boxes) for EPI_ADD_F32 (TMA reduce-add), else NULL
+cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K, int bn,
+                        int epi, const EpiArgs& ep, int num_sms, cudaStream_t s);
+bool make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems);
 int gemm_box_rows_b(int bn);
 
 // ---------------------------------------------------------------- assemble gather (k_gather.cu)
