@@ -786,6 +786,8 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
   at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
   at.n_heads = H; at.n_kv_heads = Hk; at.head_dim = dh;
   at.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
+  static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
+  at.debug_mode = attn_debug;
   if (c->attn_tc)
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
               attn_tc_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
@@ -844,7 +846,11 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   const size_t o_tok = lay.add(U * 4), o_pos = lay.add(U * 4), o_dst = lay.add(U * 4), o_cls = lay.add(U),
                o_reuse = lay.add(U), o_req = lay.add(n_req * 16), o_req2 = lay.add(n_req * 16);
   int32_t n_ut = 0, n_st = 0;
-  for (auto& p : plan) { n_ut += (p.u_cnt + TQ - 1) / TQ; n_st += (p.sel_cnt + TQ - 1) / TQ; }
+  // tile lists can be padded per request to a multiple of tpad with empty tiles (n_rows = 0) for
+  // kernels that pair consecutive tiles; the current attention kernels do not (tpad = 1)
+  const int tpad = 1;
+  auto ntiles = [&](int cnt) { const int t = (cnt + TQ - 1) / TQ; return (t + tpad - 1) / tpad * tpad; };
+  for (auto& p : plan) { n_ut += ntiles(p.u_cnt); n_st += ntiles(p.sel_cnt); }
   const size_t o_ut = lay.add(static_cast<size_t>(n_ut) * 16), o_st = lay.add(static_cast<size_t>(n_st) * 16),
                o_last = lay.add(n_req * 4), o_creq = lay.add(n_cand * 4), o_cid = lay.add(n_cand * 4),
                o_fsel = lay.add(forced ? static_cast<size_t>(S) * 12 : 0);
@@ -873,8 +879,11 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     }
     hreq[r] = make_int4(p.u_off, p.u_cnt, p.sel_off, sq.n);
     hreq2[r] = make_int4(p.k_h, p.k_i, static_cast<int>(sq.arena_row), p.window);
-    for (int i = 0; i < p.u_cnt; i += TQ) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), static_cast<int>(sq.arena_row), 0);
-    for (int i = 0; i < p.sel_cnt; i += TQ) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), static_cast<int>(sq.arena_row), 0);
+    const int arow = static_cast<int>(sq.arena_row);
+    for (int i = 0; i < p.u_cnt; i += TQ) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), arow, 0);
+    if ((ntiles(p.u_cnt) - (p.u_cnt + TQ - 1) / TQ) > 0) hut[iu++] = make_int4(p.u_off, 0, arow, 0);
+    for (int i = 0; i < p.sel_cnt; i += TQ) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), arow, 0);
+    if ((ntiles(p.sel_cnt) - (p.sel_cnt + TQ - 1) / TQ) > 0) hst[is++] = make_int4(p.sel_off, 0, arow, 0);
     H32(o_last)[r] = p.sel_off + p.sel_cnt - 1;
     for (size_t j = 0; j < sq.cand_idtok.size(); ++j) { H32(o_creq)[ic] = r; H32(o_cid)[ic] = sq.cand_idtok[j]; ++ic; }
     if (forced) {

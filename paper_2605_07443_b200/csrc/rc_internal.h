@@ -74,6 +74,7 @@ struct AttnArgs {
   int64_t head_stride;  // T_cap*dh
   int32_t n_heads, n_kv_heads, head_dim;
   float scale_log2;     // log2(e)/sqrt(dh)
+  int32_t debug_mode = 0;  // 0 = normal; 1 = skip the softmax (pipeline timing diagnostics only)
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
