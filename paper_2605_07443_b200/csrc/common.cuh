@@ -38,6 +38,12 @@ __device__ __forceinline__ unsigned long long dev_term(float a_new, uint16_t b_s
   return static_cast<unsigned long long>(__fmul_rn(y, 16777216.0f));  // exact scaling; truncation = floor
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// wait until the previous kernel in the stream has completed and its writes are visible
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// allow the next kernel in the stream to begin launching (it still waits in griddep_wait)
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

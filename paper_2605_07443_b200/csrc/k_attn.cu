@@ -49,6 +49,8 @@ __device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b
 
 template <int DH>
 __global__ void __launch_bounds__(128) k_attn(const AttnArgs a) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   using C = AttnCfg<DH>;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sQ = smem;
@@ -217,8 +219,7 @@ cudaError_t launch(const AttnArgs& a, cudaStream_t s) {
     attr = true;
   }
   dim3 grid(a.n_tiles, a.n_kv_heads);
-  k_attn<DH><<<grid, 128, C::SMEM, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_attn<DH>, dim3(grid), dim3(128), C::SMEM, s, a);
 }
 }  // namespace
 

@@ -76,16 +76,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* pv_done = p_full + 4;          // [2 halves][2] alternating per tile
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 4);
 
-  const int4 tile = a.tiles[blockIdx.x];
-  const int row_start = tile.x, n_rows = tile.y, kv_base = tile.z;
-  const int kvh = blockIdx.y;
-  const int G = a.n_heads / a.n_kv_heads;
-  const int TQ = ROWS / G;
-  const int H = a.n_heads;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int max_pos = a.qpos[row_start + n_rows - 1];
-  const int nkv = max_pos / BKV + 1;
-
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
@@ -100,6 +91,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
+  griddep_launch();
+  const int4 tile = a.tiles[blockIdx.x];
+  const int row_start = tile.x, n_rows = tile.y, kv_base = tile.z;
+  const int kvh = blockIdx.y;
+  const int G = a.n_heads / a.n_kv_heads;
+  const int TQ = ROWS / G;
+  const int H = a.n_heads;
+  const int max_pos = a.qpos[row_start + n_rows - 1];
+  const int nkv_all = max_pos / BKV + 1;
+  const int j0 = tile.w * nkv_all / a.n_splits;         // this split's KV tiles [j0, j0 + nkv)
+  const int nkv = (tile.w + 1) * nkv_all / a.n_splits - j0;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- Q + K producer
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_expect_tx(q_full, 2u * 128u * G * TQ);
       tma_load_3d(sQ, &tmQ, q_full, 0, kvh * G, row_start);
       tma_load_3d(sQ + HALF, &tmQ, q_full, 64, kvh * G, row_start);
-      const int krow0 = static_cast<int>(kvh * t_cap + kv_base);
+      const int krow0 = static_cast<int>(kvh * t_cap + kv_base) + j0 * BKV;
       for (int j = 0; j < nkv; ++j) {
         const int s = j % KST;
         mbar_wait(&k_empty[s], ((j / KST) & 1) ^ 1);
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == 3) {
     if (lane == 0) {  // ---- V producer
       tma_prefetch_desc(&tmV);
-      const int vrow0 = static_cast<int>(kvh * t_cap + kv_base);
+      const int vrow0 = static_cast<int>(kvh * t_cap + kv_base) + j0 * BKV;
       for (int j = 0; j < nkv; ++j) {
         const int s = j % VST;
         mbar_wait(&v_empty[s], ((j / VST) & 1) ^ 1);
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         umma_commit(&k_empty[s]);
         umma_commit(&s_full[j & 1]);
       };
-      issue_s(0);
+      if (nkv > 0) issue_s(0);
       if (nkv > 1) issue_s(1);
       for (int j = 0; j < nkv; ++j) {
         const int b = j & 1, v = j % VST;
@@ -187,9 +190,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_ld32(tmem + lane_base + b * 128 + col0, sr);
       tmem_ld32(tmem + lane_base + b * 128 + col0 + 32, sr + 32);
       tmem_wait_ld();
-      const int key0 = j * BKV + col0;
+      const int key0 = (j0 + j) * BKV + col0;
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
-      if (j * BKV + BKV - 1 <= p_first) {  // every row of the tile sees every key: no causal mask
+      if ((j0 + j) * BKV + BKV - 1 <= p_first) {  // every row of the tile sees every key: no causal mask
 #pragma unroll
         for (int c = 0; c < SCOLS; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sr[c]));
       } else {
@@ -259,26 +262,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const float l_tot = l0 * f0 + l1 * f1;
     const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
     const float w0 = f0 * inv, w1 = f1 * inv;
-    mbar_wait(&pv_done[0 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
-    mbar_wait(&pv_done[1 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
+    if (nkv > 0) {
+      mbar_wait(&pv_done[0 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
+      mbar_wait(&pv_done[1 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
+    }
     tc_fence_after();
-    // this thread writes output columns [h*64, h*64 + 64) of its row
+    const bool split = a.n_splits > 1;
+    // this thread writes output columns [h*64, h*64 + 64) of its row: bf16 into o, or (KV split) the
+    // fp32 partial normalised by its own l plus (m, l) for the merge kernel
     uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + h * 64;
+    const int64_t prow = (static_cast<int64_t>(blockIdx.x) * a.n_kv_heads + kvh) * ROWS + r;
+    float* pdst = split ? a.part_o + prow * DH + h * 64 : nullptr;
+    if (split && h == 0) {
+      a.part_ml[prow * 2] = m;
+      a.part_ml[prow * 2 + 1] = nkv > 0 ? l_tot : 0.f;
+    }
 #pragma unroll
     for (int c = 0; c < 64; c += 32) {
       uint32_t o0[32], o1[32];
-      tmem_ld32(tmem + lane_base + O_COL + h * 64 + c, o0);
-      tmem_ld32(tmem + lane_base + O_COL + 128 + h * 64 + c, o1);
-      tmem_wait_ld();
+      if (nkv > 0) {
+        tmem_ld32(tmem + lane_base + O_COL + h * 64 + c, o0);
+        tmem_ld32(tmem + lane_base + O_COL + 128 + h * 64 + c, o1);
+        tmem_wait_ld();
+      }
       if (valid) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           float y[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) y[k] = __uint_as_float(o0[i + k]) * w0 + __uint_as_float(o1[i + k]) * w1;
-          uint4 u;
-          u.x = pack_bf2(y[0], y[1]); u.y = pack_bf2(y[2], y[3]); u.z = pack_bf2(y[4], y[5]); u.w = pack_bf2(y[6], y[7]);
-          *reinterpret_cast<uint4*>(dst + c + i) = u;
+          for (int k = 0; k < 8; ++k)
+            y[k] = nkv > 0 ? __uint_as_float(o0[i + k]) * w0 + __uint_as_float(o1[i + k]) * w1 : 0.f;
+          if (split) {
+            reinterpret_cast<float4*>(pdst + c + i)[0] = make_float4(y[0], y[1], y[2], y[3]);
+            reinterpret_cast<float4*>(pdst + c + i)[1] = make_float4(y[4], y[5], y[6], y[7]);
+          } else {
+            uint4 u;
+            u.x = pack_bf2(y[0], y[1]); u.y = pack_bf2(y[2], y[3]); u.z = pack_bf2(y[4], y[5]); u.w = pack_bf2(y[6], y[7]);
+            *reinterpret_cast<uint4*>(dst + c + i) = u;
+          }
         }
       }
     }
@@ -287,6 +308,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
+// KV-split merge: out = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - max m). One thread per
+// (row, 8-column chunk) of a logical query tile; splits with l_s = 0 (no visible keys) are skipped.
+__global__ void __launch_bounds__(256) k_attn_merge(const AttnArgs a) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
+  const int t_log = blockIdx.x, kvh = blockIdx.y, S = a.n_splits;
+  const int4 tile = a.tiles[t_log * S];
+  const int G = a.n_heads / a.n_kv_heads, TQ = ROWS / G;
+  // blockIdx.z picks a 16-row slab: 16 rows x 16 chunks = one unit per thread, so every split's
+  // partial is loaded in one round trip (the merge is latency-, not bandwidth-bound)
+  const int r = blockIdx.z * 16 + threadIdx.x / (DH / 8), c = (threadIdx.x % (DH / 8)) * 8;
+  const int t = r / G, g = r % G;
+  if (r >= TQ * G || t >= tile.y) return;
+  float ml[2 * 8];
+  float4 x[2 * 8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s < S) {
+      const int64_t prow = (static_cast<int64_t>(t_log * S + s) * a.n_kv_heads + kvh) * ROWS + r;
+      const float2 v = *reinterpret_cast<const float2*>(a.part_ml + prow * 2);
+      ml[2 * s] = v.x; ml[2 * s + 1] = v.y;
+      x[2 * s] = reinterpret_cast<const float4*>(a.part_o + prow * DH + c)[0];
+      x[2 * s + 1] = reinterpret_cast<const float4*>(a.part_o + prow * DH + c)[1];
+    }
+  }
+  float m = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    if (s < S && ml[2 * s + 1] > 0.f) m = fmaxf(m, ml[2 * s]);
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    if (s >= S || !(ml[2 * s + 1] > 0.f)) continue;
+    const float w = ml[2 * s + 1] * fast_exp2(ml[2 * s] - m);
+    const float4 x0 = x[2 * s], x1 = x[2 * s + 1];
+    acc[0] += w * x0.x; acc[1] += w * x0.y; acc[2] += w * x0.z; acc[3] += w * x0.w;
+    acc[4] += w * x1.x; acc[5] += w * x1.y; acc[6] += w * x1.z; acc[7] += w * x1.w;
+    wsum += w;
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  uint4 u;
+  u.x = pack_bf2(acc[0] * inv, acc[1] * inv); u.y = pack_bf2(acc[2] * inv, acc[3] * inv);
+  u.z = pack_bf2(acc[4] * inv, acc[5] * inv); u.w = pack_bf2(acc[6] * inv, acc[7] * inv);
+  *reinterpret_cast<uint4*>(a.o + static_cast<int64_t>(tile.x + t) * a.n_heads * DH + (kvh * G + g) * DH + c) = u;
 }
 }  // namespace
 
@@ -302,8 +369,25 @@ cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const
     attr = true;
   }
   dim3 grid(a.n_tiles, a.n_kv_heads);
-  k_attn_tc<<<grid, NTHREADS, SMEM_BYTES, s>>>(*tmQ, *tmK, *tmV, a, t_cap);
-  return cudaGetLastError();
+  cudaError_t e = launch_pdl(k_attn_tc, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV, a, t_cap);
+  if (e != cudaSuccess || a.n_splits <= 1) return e;
+  return launch_pdl(k_attn_merge, dim3(a.n_tiles / a.n_splits, a.n_kv_heads, ROWS / 16), dim3(256), 0, s, a);
+}
+
+int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms) {
+  // Split only grids that leave more than half the machine idle. Measured at cfg3 batch 1 (176
+  // CTAs, ~1.2 waves): a uniform 2-way split costs +0.35 ms over 32 launches, because the split
+  // shares are uniform while the causal KV lengths are not and the extra partial write + merge
+  // outweigh the shorter critical path.
+  static const int forced = [] {
+    const char* e = getenv("RC_ATTN_SPLITS");  // diagnostics: force a split count (1 = off)
+    return e ? atoi(e) : 0;
+  }();
+  if (forced >= 1 && forced <= 8) return forced;
+  const int64_t units = static_cast<int64_t>(n_tiles) * n_kv_heads;
+  int best = 1;
+  while (best < 8 && units * (best * 2) <= num_sms && est_kv_tiles / (best * 2) >= 4) best *= 2;
+  return best;
 }
 
 }  // namespace rc

@@ -47,6 +47,8 @@ struct Unit {
 
 template <int DH>
 __global__ void __launch_bounds__(256) k_gather(const GatherArgs g) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   constexpr int HALF = DH / 2, CPR = DH / 16;
   const int nl = g.layer_end - g.layer_begin;
   const int Hk = g.n_kv_heads;
@@ -151,8 +153,7 @@ cudaError_t launch(const GatherArgs& g, int num_sms, cudaStream_t s) {
   const int64_t want = (static_cast<int64_t>(num_sms) * per_sm * 8 + planes - 1) / planes;
   if (bx > want) bx = want;
   if (bx < 1) bx = 1;
-  k_gather<DH><<<dim3(static_cast<unsigned>(bx), planes), 256, 0, s>>>(g);
-  return cudaGetLastError();
+  return launch_pdl(k_gather<DH>, dim3(static_cast<unsigned>(bx), planes), dim3(256), 0, s, g);
 }
 }  // namespace
 

@@ -282,6 +282,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
+  griddep_launch();
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
@@ -382,8 +384,7 @@ cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, const CUtenso
   }
   const int units = tiles * splits;
   const int grid = units < num_sms ? units : num_sms;
-  k_gemm<BN, EPI><<<grid, 256, C::SMEM, s>>>(*a, *b, c ? *c : *a, M, N, K, splits, ep);
-  return cudaGetLastError();
+  return launch_pdl(k_gemm<BN, EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits, ep);
 }
 
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

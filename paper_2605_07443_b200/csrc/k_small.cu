@@ -16,6 +16,8 @@ enum { CLS_PREFIX = 0, CLS_FORCED = 1, CLS_HIST = 2, CLS_ITEM = 3 };
 
 __global__ void k_embed(const uint16_t* __restrict__ emb, const int32_t* __restrict__ tok, int32_t rows, int32_t d,
                         float* __restrict__ x) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int64_t n8 = static_cast<int64_t>(rows) * (d / 8);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -35,6 +37,8 @@ __global__ void k_embed(const uint16_t* __restrict__ emb, const int32_t* __restr
 __global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, const int32_t* __restrict__ row_idx,
                                                  int32_t d, const uint16_t* __restrict__ g, float eps,
                                                  uint16_t* __restrict__ out) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   __shared__ float red[8];
   const int r = blockIdx.x;
   const int64_t src = row_idx ? row_idx[r] : r;
@@ -70,6 +74,8 @@ __global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, co
 
 __global__ void k_gather_rows(const float* __restrict__ src, const int32_t* __restrict__ idx, int32_t rows, int32_t d,
                               float* __restrict__ dst) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int64_t n4 = static_cast<int64_t>(rows) * (d / 4);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -88,6 +94,8 @@ __device__ __forceinline__ unsigned long long sel_key(unsigned long long dev, in
 }
 
 __global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   __shared__ uint8_t flag[SEL_MAX_U];
   __shared__ uint8_t cls[SEL_MAX_U];
   __shared__ int hist[256];
@@ -177,6 +185,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
 
 __global__ void k_cand_scores(const float* logits, int64_t vocab, const int32_t* cand_req, const int32_t* idtok, int32_t n,
                               float* out) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = logits[static_cast<int64_t>(cand_req[i]) * vocab + idtok[i]];
 }
@@ -184,6 +194,8 @@ __global__ void k_cand_scores(const float* logits, int64_t vocab, const int32_t*
 // [n_tok][L][2][Hk][dh] -> [L][2][Hk][dst_rows][dh] at rows dst_row0 + t (16-byte chunks)
 __global__ void k_pool_transpose(const uint8_t* __restrict__ src, int eb, int32_t n_tok, int32_t L, int32_t Hk,
                                  int32_t dh, uint8_t* __restrict__ dst, int64_t dst_rows, int64_t dst_row0) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int row_bytes = dh * eb;
   const int cpr = row_bytes / 16;
   const int64_t units = static_cast<int64_t>(n_tok) * L * 2 * Hk * cpr;
@@ -200,6 +212,8 @@ __global__ void k_pool_transpose(const uint8_t* __restrict__ src, int eb, int32_
 
 __global__ void k_scale_transpose(const float* __restrict__ src, int32_t n_tok, int32_t planes, float* __restrict__ dst,
                                   int64_t dst_rows, int64_t dst_row0) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int64_t units = static_cast<int64_t>(n_tok) * planes;
   for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
        u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -212,6 +226,8 @@ __global__ void k_scale_transpose(const float* __restrict__ src, int32_t n_tok, 
 // mapped peer pool: one-sided NVLink reads) -> [planes][dst_rows] at dst_row0
 __global__ void k_copy_rows(const uint8_t* __restrict__ src, int64_t src_rows, int64_t src_row0, uint8_t* __restrict__ dst,
                             int64_t dst_rows, int64_t dst_row0, int32_t n_rows, int32_t planes, int32_t row_bytes) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int cpr = row_bytes / 16;
   const int64_t units = static_cast<int64_t>(planes) * n_rows * cpr;
   for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
@@ -226,6 +242,8 @@ __global__ void k_copy_rows(const uint8_t* __restrict__ src, int64_t src_rows, i
 
 __global__ void k_read_kv(const uint16_t* __restrict__ arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
                           int32_t row0, int32_t n, uint16_t* __restrict__ k_out, uint16_t* __restrict__ v_out) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int64_t units = static_cast<int64_t>(2) * n * Hk * dh;
   for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
        u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -243,6 +261,8 @@ __global__ void k_read_kv(const uint16_t* __restrict__ arena, int64_t arena_rows
 // diagnostic K5: D[i] = sum_j term(k_new, k_st) + term(v_new, v_st) over `width` elements, one warp per row
 __global__ void k_dev_diag(const uint16_t* kn, const uint16_t* ks, const uint16_t* vn, const uint16_t* vs, int32_t n,
                            int32_t width, unsigned long long* out) {
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
@@ -266,71 +286,61 @@ inline int blocks_for(int64_t units, int per = 256, int cap = 148 * 16) {
 
 cudaError_t embed_launch(const uint16_t* emb, const int32_t* tok, int32_t rows, int32_t d, float* x, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  k_embed<<<blocks_for(static_cast<int64_t>(rows) * d / 8), 256, 0, s>>>(emb, tok, rows, d, x);
-  return cudaGetLastError();
+  return launch_pdl(k_embed, dim3(blocks_for(static_cast<int64_t>(rows) * d / 8)), dim3(256), 0, s, emb, tok, rows, d, x);
 }
 cudaError_t rmsnorm_launch(const float* x, const int32_t* row_idx, int32_t rows, int32_t d, const uint16_t* g, float eps,
                            uint16_t* out, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
   const int th = d >= 1024 ? 256 : 64;
-  k_rmsnorm<<<rows, th, 0, s>>>(x, row_idx, d, g, eps, out);
-  return cudaGetLastError();
+  return launch_pdl(k_rmsnorm, dim3(rows), dim3(th), 0, s, x, row_idx, d, g, eps, out);
 }
 cudaError_t gather_rows_f32_launch(const float* src, const int32_t* idx, int32_t rows, int32_t d, float* dst,
                                    cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  k_gather_rows<<<blocks_for(static_cast<int64_t>(rows) * d / 4), 256, 0, s>>>(src, idx, rows, d, dst);
-  return cudaGetLastError();
+  return launch_pdl(k_gather_rows, dim3(blocks_for(static_cast<int64_t>(rows) * d / 4)), dim3(256), 0, s, src, idx, rows, d, dst);
 }
 cudaError_t select_launch(const SelectArgs& a, cudaStream_t s) {
   if (a.n_req <= 0) return cudaSuccess;
-  k_select<<<a.n_req, SEL_THREADS, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_select, dim3(a.n_req), dim3(SEL_THREADS), 0, s, a);
 }
 cudaError_t dev_diag_launch(const uint16_t* kn, const uint16_t* ks, const uint16_t* vn, const uint16_t* vs, int32_t n,
                             int32_t width, unsigned long long* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_dev_diag<<<(n + 7) / 8, 256, 0, s>>>(kn, ks, vn, vs, n, width, out);
-  return cudaGetLastError();
+  return launch_pdl(k_dev_diag, dim3((n + 7) / 8), dim3(256), 0, s, kn, ks, vn, vs, n, width, out);
 }
 cudaError_t cand_scores_launch(const float* logits, int64_t vocab, const int32_t* cand_req, const int32_t* idtok,
                                int32_t n, float* out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_cand_scores<<<(n + 255) / 256, 256, 0, s>>>(logits, vocab, cand_req, idtok, n, out);
-  return cudaGetLastError();
+  return launch_pdl(k_cand_scores, dim3((n + 255) / 256), dim3(256), 0, s, logits, vocab, cand_req, idtok, n, out);
 }
 cudaError_t pool_transpose_launch(const void* src, int eb, int32_t n_tok, int32_t L, int32_t Hk, int32_t dh, void* dst,
                                   int64_t dst_rows, int64_t dst_row0, cudaStream_t s) {
   if (n_tok <= 0) return cudaSuccess;
   if ((dh * eb) % 16) return cudaErrorInvalidValue;
   const int64_t units = static_cast<int64_t>(n_tok) * L * 2 * Hk * (dh * eb / 16);
-  k_pool_transpose<<<blocks_for(units), 256, 0, s>>>(static_cast<const uint8_t*>(src), eb, n_tok, L, Hk, dh,
+  return launch_pdl(k_pool_transpose, dim3(blocks_for(units)), dim3(256), 0, s, static_cast<const uint8_t*>(src), eb, n_tok, L, Hk, dh,
                                                      static_cast<uint8_t*>(dst), dst_rows, dst_row0);
-  return cudaGetLastError();
 }
 cudaError_t scale_transpose_launch(const float* src, int32_t n_tok, int32_t L, int32_t Hk, float* dst, int64_t dst_rows,
                                    int64_t dst_row0, cudaStream_t s) {
   if (n_tok <= 0) return cudaSuccess;
-  k_scale_transpose<<<blocks_for(static_cast<int64_t>(n_tok) * L * 2 * Hk), 256, 0, s>>>(src, n_tok, L * 2 * Hk, dst,
+  return launch_pdl(k_scale_transpose, dim3(blocks_for(static_cast<int64_t>(n_tok) * L * 2 * Hk)), dim3(256), 0, s, src, n_tok, L * 2 * Hk, dst,
                                                                                          dst_rows, dst_row0);
-  return cudaGetLastError();
 }
 cudaError_t copy_rows_launch(const void* src_base, int64_t src_rows, int64_t src_row0, void* dst_base, int64_t dst_rows,
                              int64_t dst_row0, int32_t n_rows, int32_t n_planes, int32_t row_bytes, cudaStream_t s) {
   if (n_rows <= 0) return cudaSuccess;
   if (row_bytes % 16) return cudaErrorInvalidValue;
   const int64_t units = static_cast<int64_t>(n_planes) * n_rows * (row_bytes / 16);
-  k_copy_rows<<<blocks_for(units), 256, 0, s>>>(static_cast<const uint8_t*>(src_base), src_rows, src_row0,
+  return launch_pdl(k_copy_rows, dim3(blocks_for(units)), dim3(256), 0, s, static_cast<const uint8_t*>(src_base), src_rows, src_row0,
                                                 static_cast<uint8_t*>(dst_base), dst_rows, dst_row0, n_rows, n_planes,
                                                 row_bytes);
-  return cudaGetLastError();
 }
 cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh, int32_t row0,
                            int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  k_read_kv<<<blocks_for(static_cast<int64_t>(2) * n * Hk * dh), 256, 0, s>>>(arena, arena_rows, layer, Hk, dh, row0, n,
+  return launch_pdl(k_read_kv, dim3(blocks_for(static_cast<int64_t>(2) * n * Hk * dh)), dim3(256), 0, s, arena, arena_rows, layer, Hk, dh, row0, n,
                                                                              k_out, v_out);
-  return cudaGetLastError();
 }
 
 }  // namespace rc

@@ -26,6 +26,14 @@ int32_t rc::set_error(int32_t code, const char* msg) {
   return code;
 }
 
+bool rc::pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 rc_status fail(rc_status code, const std::string& msg) {
@@ -199,6 +207,9 @@ struct rc_ctx {
   unsigned long long* dev = nullptr;
   float* logits = nullptr;
   int64_t logits_rows = 0;
+  float* part_o = nullptr;   // KV-split attention partials
+  float* part_ml = nullptr;
+  size_t part_rows = 0;
   int32_t* sel_pos = nullptr;
   int32_t* sel_dst = nullptr;
   int32_t* sel_urow = nullptr;
@@ -230,7 +241,7 @@ struct rc_ctx {
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
-                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow};
+                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml};
     for (void* p : bufs)
       if (p) cudaFree(p);
   }
@@ -765,8 +776,8 @@ rc_status rc_sel_count(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_pr
 namespace {
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
 rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
-                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, double attn_flops, int attn_pending,
-                    cudaStream_t s) {
+                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, double attn_flops,
+                    int attn_pending, cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
   const double R = rows, norm_b = R * d * 6.0;
@@ -788,6 +799,22 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
   at.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
   static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
   at.debug_mode = attn_debug;
+  at.n_splits = n_splits;
+  if (n_splits > 1) {  // partial-output workspace, grown on first use
+    const size_t need = static_cast<size_t>(n_tiles) * Hk * 128;
+    if (c->part_rows < need) {
+      if (c->part_o) cudaFree(c->part_o);
+      if (c->part_ml) cudaFree(c->part_ml);
+      cudaError_t e;
+      c->part_o = dev_alloc<float>(need * 128, &e);
+      if (e == cudaSuccess) c->part_ml = dev_alloc<float>(need * 2, &e);
+      if (e != cudaSuccess) { c->part_rows = 0; return fail(RC_E_NOMEM, "attention split workspace"); }
+      c->part_rows = need;
+    }
+    at.part_o = c->part_o;
+    at.part_ml = c->part_ml;
+    c->launches += 1;  // the merge kernel
+  }
   if (c->attn_tc)
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
               attn_tc_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
@@ -846,11 +873,20 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   const size_t o_tok = lay.add(U * 4), o_pos = lay.add(U * 4), o_dst = lay.add(U * 4), o_cls = lay.add(U),
                o_reuse = lay.add(U), o_req = lay.add(n_req * 16), o_req2 = lay.add(n_req * 16);
   int32_t n_ut = 0, n_st = 0;
-  // tile lists can be padded per request to a multiple of tpad with empty tiles (n_rows = 0) for
-  // kernels that pair consecutive tiles; the current attention kernels do not (tpad = 1)
-  const int tpad = 1;
-  auto ntiles = [&](int cnt) { const int t = (cnt + TQ - 1) / TQ; return (t + tpad - 1) / tpad * tpad; };
+  auto ntiles = [&](int cnt) { return (cnt + TQ - 1) / TQ; };
   for (auto& p : plan) { n_ut += ntiles(p.u_cnt); n_st += ntiles(p.sel_cnt); }
+  // small grids (e.g. one request's selected rows) fill the SMs badly: split the KV range of every
+  // query tile over several CTAs and merge (tcgen05 kernel only); every entry repeats per split
+  int split_u = 1, split_s = 1;
+  if (c->attn_tc) {
+    int64_t ntok = 0;
+    for (auto& p : plan) ntok += p.sq->n;
+    const int est_kv = static_cast<int>(ntok / n_req / 128) + 1;
+    split_u = attn_tc_choose_splits(n_ut, m.n_kv_heads, est_kv, c->num_sms);
+    split_s = attn_tc_choose_splits(n_st, m.n_kv_heads, est_kv, c->num_sms);
+  }
+  n_ut *= split_u;
+  n_st *= split_s;
   const size_t o_ut = lay.add(static_cast<size_t>(n_ut) * 16), o_st = lay.add(static_cast<size_t>(n_st) * 16),
                o_last = lay.add(n_req * 4), o_creq = lay.add(n_cand * 4), o_cid = lay.add(n_cand * 4),
                o_fsel = lay.add(forced ? static_cast<size_t>(S) * 12 : 0);
@@ -880,10 +916,10 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     hreq[r] = make_int4(p.u_off, p.u_cnt, p.sel_off, sq.n);
     hreq2[r] = make_int4(p.k_h, p.k_i, static_cast<int>(sq.arena_row), p.window);
     const int arow = static_cast<int>(sq.arena_row);
-    for (int i = 0; i < p.u_cnt; i += TQ) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), arow, 0);
-    if ((ntiles(p.u_cnt) - (p.u_cnt + TQ - 1) / TQ) > 0) hut[iu++] = make_int4(p.u_off, 0, arow, 0);
-    for (int i = 0; i < p.sel_cnt; i += TQ) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), arow, 0);
-    if ((ntiles(p.sel_cnt) - (p.sel_cnt + TQ - 1) / TQ) > 0) hst[is++] = make_int4(p.sel_off, 0, arow, 0);
+    for (int i = 0; i < p.u_cnt; i += TQ)
+      for (int sp = 0; sp < split_u; ++sp) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), arow, sp);
+    for (int i = 0; i < p.sel_cnt; i += TQ)
+      for (int sp = 0; sp < split_s; ++sp) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), arow, sp);
     H32(o_last)[r] = p.sel_off + p.sel_cnt - 1;
     for (size_t j = 0; j < sq.cand_idtok.size(); ++j) { H32(o_creq)[ic] = r; H32(o_cid)[ic] = sq.cand_idtok[j]; ++ic; }
     if (forced) {
@@ -910,7 +946,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   attn_u *= 4.0 * m.n_heads * m.head_dim;
   const int pend_idx = c->prof ? static_cast<int>(c->pend.size()) : -1;
   for (int l = 0; l < cL; ++l) {
-    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, attn_u, -1, s);
+    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, attn_u, -1, s);
     if (st != RC_OK) return st;
   }
   // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
@@ -946,7 +982,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
             gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
   // ---- a5-a7: selective layers c..L-1 on Sel
   for (int l = cL; l < L; ++l) {
-    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, 0.0, pend_idx, s);
+    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, 0.0, pend_idx, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout

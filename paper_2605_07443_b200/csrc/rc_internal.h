@@ -9,6 +9,26 @@ namespace rc {
 // sets the thread-local message returned by rc_last_error(); returns code
 int32_t set_error(int32_t code, const char* msg);
 
+// Every hot-path kernel is launched with programmatic dependent launch (PDL): it may start while
+// the previous kernel in the stream drains, runs its prologue (barrier init, TMEM allocation,
+// descriptor prefetch), and blocks in griddepcontrol.wait before touching memory the previous
+// kernel produced. Kernels call griddepcontrol.launch_dependents once all their CTAs are running.
+bool pdl_enabled();  // RC_PDL=0 in the environment turns the attribute off (A/B diagnostics)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- dense GEMM (tcgen05, k_gemm.cu)
 // C[M][N] = A[M][K] * B[N][K]^T, A and B bf16 K-major, fp32 accumulation in TMEM; the epilogue
 // decides what happens to each fp32 accumulator row.
@@ -75,12 +95,19 @@ struct AttnArgs {
   int32_t n_heads, n_kv_heads, head_dim;
   float scale_log2;     // log2(e)/sqrt(dh)
   int32_t debug_mode = 0;  // 0 = normal; 1 = skip the softmax (pipeline timing diagnostics only)
+  // KV split (tcgen05 kernel): tiles[] holds n_splits consecutive entries per query tile, .w = split
+  // index; each covers a contiguous share of the KV tiles and writes a partial (normalised O, m, l)
+  // that a merge kernel combines (small grids only; n_splits = 1 writes o directly)
+  int32_t n_splits = 1;
+  float* part_o = nullptr;   // [n_tiles][Hk][128][128]
+  float* part_ml = nullptr;  // [n_tiles][Hk][128][2]
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
 // tcgen05 version (head_dim == 128): 128-row tiles, Q via a 3-D tensor map over q [R][H][dh],
 // K/V via 2-D maps over the layer's arena [Hk*T_cap][dh] (k_attn_tc.cu)
 int attn_tc_tokens_per_tile(int group);
+int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms);
 cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV, const AttnArgs& a,
                            int64_t t_cap, cudaStream_t s);
 bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
