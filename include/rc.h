@@ -127,7 +127,11 @@ typedef struct rc_prefill_params {
   const int32_t* forced_sel;  /* optional host list: Sel positions per request, concatenated,
                                  ascending, must contain every FORCED position (test mode)   */
   const int32_t* forced_sel_off; /* [n_req+1] offsets into forced_sel (with forced_sel)      */
+  int32_t attn_kernel;        /* attention launch shape (d_h = 128): RC_ATTN_AUTO chooses by grid
+                                 size; the others force one (tests). Results agree within the
+                                 rounding of the online softmax, not bit for bit */
 } rc_prefill_params;
+enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3 };
 
 /* ---------------------------------------------------------------- lifecycle */
 rc_status rc_create(const rc_model_desc* m, const rc_weights* w, const rc_pool_desc* p, int32_t device,

@@ -123,8 +123,8 @@ class RcContext:
         check(code)
         return seqs
 
-    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0):
-        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None)
+    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0, attn_kernel=0):
+        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None, attn_kernel)
         keep = None
         if forced_sel is not None:
             off = np.zeros(len(forced_sel) + 1, np.int32)
@@ -144,11 +144,11 @@ class RcContext:
 
     def selective_prefill(self, seqs, r_rev_bp, r_item_bp, check_layer=1, window=0, forced_sel=None, lam=1.0,
                           logits=True, cand_scores=True, sel_pos=True, hidden=False, n_cand=None, out=None,
-                          stream=None):
+                          stream=None, attn_kernel=0):
         """Returns dict of CUDA tensors (logits, cand_scores, sel_pos, hidden) as requested. `out`
         may hold preallocated tensors with the same keys (reused; no allocation)."""
         seqs = np.ascontiguousarray(seqs, np.uint64)
-        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam)
+        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam, attn_kernel)
         dev = torch.device("cuda", self.device)
         res = dict(out) if out else {}
         if (sel_pos or hidden) and ("sel_pos" not in res and "hidden" not in res):

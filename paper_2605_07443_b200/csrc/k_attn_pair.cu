@@ -1,0 +1,322 @@
+// K4/K7 on tcgen05, paired query tiles (d_h = 128): causal attention of query tokens over their
+// request's stitched KV (Eq. 1; R11). Used for large grids
+// (batch 32: thousands of tiles), where the single-tile kernel (k_attn_tc.cu) is bound by the L2->SM
+// stream of K/V tiles: every K/V tile is fetched once per 128 query rows.
+//
+// CTA = (two query tiles of ONE request, kv head): Q_0, Q_1 stay in shared memory and every K/V tile
+// is loaded once for both, halving the K/V bytes per FLOP. Tile t <-> TMEM S_t (columns 128 t) and
+// O_t (columns 256 + 128 t); row r of a tile <-> TMEM lane r.
+//   warp 0 lane 0   TMA: Q_0, Q_1 once (3-D boxes [TQ][G][64] x 2 halves), K tiles (2-stage ring)
+//   warp 3 lane 0   TMA: V tiles (2-stage ring)
+//   warp 1 lane 0   MMA, ping-pong over the two tiles: after softmax t has turned S_t(j) into P_t(j)
+//                   it issues O_t += P_t(j) V_j (TS mode, A = P from TMEM) and immediately
+//                   S_t(j+1) = Q_t K_{j+1}^T, so the tensor pipe works on one tile while the other
+//                   tile's softmax runs. In-order execution of one thread's MMAs makes the reuse of
+//                   S_t's columns safe, and the commit of S_t(j+1) also covers PV_t(j).
+//   warps 4-7 / 8-11  softmax of tile 0 / tile 1: thread <-> query row; each 128-key tile in two
+//                   64-key halves (tcgen05.ld of the half, causal mask by true position unless the
+//                   whole tile is visible, lazy rescale when the running max grows by > 2^8, P in
+//                   bf16 pairs written back over the S columns already consumed). If the second
+//                   half raises the running max, the first half's stored P is rescaled in TMEM (rare).
+// Tiles: a.tiles holds 2 consecutive entries per CTA, both of the same request (the host pads a
+// request's odd tile count with an empty tile {row, 0, kv_base, 0}).
+#include "common.cuh"
+#include "rc_internal.h"
+
+namespace rc {
+namespace {
+
+constexpr int DH = 128, BKV = 128, ROWS = 128;
+constexpr uint32_t HALF = ROWS * 64 * 2;  // one [128 rows][64 bf16] SW128 sub-tile = 16 KB
+constexpr uint32_t TILE = 2 * HALF;       // 32 KB
+constexpr int NTHREADS = 128 + 256;       // 4 control warps + 2 x 4 softmax warps
+constexpr int KST = 2, VST = 2;
+constexpr uint32_t OFF_Q = 0, OFF_K = 2 * TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
+constexpr uint32_t O_COL = 256;            // O_t at 256 + 128 t
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_attn_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int64_t t_cap) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0) __trap();
+  uint8_t* sQ = smem + OFF_Q;
+  uint8_t* sK = smem + OFF_K;
+  uint8_t* sV = smem + OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* q_full = bars;           // [1]
+  uint64_t* k_full = bars + 1;       // [KST]
+  uint64_t* k_empty = k_full + KST;  // [KST]
+  uint64_t* v_full = k_empty + KST;  // [VST]
+  uint64_t* v_empty = v_full + VST;  // [VST]
+  uint64_t* s_full = v_empty + VST;  // [2 tiles]
+  uint64_t* p_full = s_full + 2;     // [2 tiles]
+  uint64_t* o_done = p_full + 2;     // [2 tiles] last PV of the tile complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int t = 0; t < 2; ++t) { mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 128); mbar_init(&o_done[t], 1); }
+    fence_barrier_init();
+    fence_proxy_async();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
+  griddep_launch();
+
+  const int kvh = blockIdx.y;
+  const int G = a.n_heads / a.n_kv_heads;
+  const int TQ = ROWS / G;
+  const int H = a.n_heads;
+  int4 tl[2];
+  int nk[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    tl[t] = a.tiles[2 * blockIdx.x + t];
+    nk[t] = tl[t].y > 0 ? a.qpos[tl[t].x + tl[t].y - 1] / BKV + 1 : 0;  // rows sorted by position
+  }
+  const int nkv = max(nk[0], nk[1]);
+  const int kv_base = tl[0].z;
+
+  if (warp == 0) {
+    if (lane == 0 && nkv > 0) {  // ---- Q + K producer
+      tma_prefetch_desc(&tmQ); tma_prefetch_desc(&tmK);
+      mbar_expect_tx(q_full, ((nk[0] > 0 ? 1u : 0u) + (nk[1] > 0 ? 1u : 0u)) * 2u * 128u * G * TQ);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (nk[t] == 0) continue;
+        tma_load_3d(sQ + t * TILE, &tmQ, q_full, 0, kvh * G, tl[t].x);
+        tma_load_3d(sQ + t * TILE + HALF, &tmQ, q_full, 64, kvh * G, tl[t].x);
+      }
+      const int krow0 = static_cast<int>(kvh * t_cap + kv_base);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % KST;
+        mbar_wait(&k_empty[s], ((j / KST) & 1) ^ 1);
+        mbar_expect_tx(&k_full[s], TILE);
+        tma_load_2d(sK + s * TILE, &tmK, &k_full[s], 0, krow0 + j * BKV);
+        tma_load_2d(sK + s * TILE + HALF, &tmK, &k_full[s], 64, krow0 + j * BKV);
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0 && nkv > 0) {  // ---- V producer
+      tma_prefetch_desc(&tmV);
+      const int vrow0 = static_cast<int>(kvh * t_cap + kv_base);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % VST;
+        mbar_wait(&v_empty[s], ((j / VST) & 1) ^ 1);
+        mbar_expect_tx(&v_full[s], TILE);
+        tma_load_2d(sV + s * TILE, &tmV, &v_full[s], 0, vrow0 + j * BKV);
+        tma_load_2d(sV + s * TILE + HALF, &tmV, &v_full[s], 64, vrow0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nkv > 0) {  // ---- MMA issuer
+      constexpr uint32_t idS = idesc_bf16_f32(128, 128);
+      constexpr uint32_t idPV = idesc_bf16_f32_bmn(128, 128);
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      auto wait_k = [&](int j) {
+        mbar_wait(&k_full[j % KST], (j / KST) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+        const int s = j % KST;
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const uint64_t ad = sdesc_sw128(smem_u32(sQ + t * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
+          const uint64_t bd = sdesc_sw128(smem_u32(sK + s * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
+          umma_bf16(tmem + t * 128, ad, bd, idS, k > 0);
+        }
+        umma_commit(&s_full[t]);
+      };
+      wait_k(0);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (nk[t] > 0) issue_s(t, 0);
+      umma_commit(&k_empty[0]);
+      for (int j = 0; j < nkv; ++j) {
+        const int v = j % VST;
+        mbar_wait(&v_full[v], (j / VST) & 1);
+        tc_fence_after();
+        bool k_ready = false;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (j >= nk[t]) continue;
+          mbar_wait(&p_full[t], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int k = 0; k < BKV / 16; ++k) {  // 16 keys per MMA: A = P_t (8 TMEM columns), B = V rows
+            const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + v * TILE + k * 2048), HALF, 1024);
+            umma_bf16_ts(tmem + O_COL + t * 128, tmem + t * 128 + k * 8, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
+          }
+          if (j + 1 == nk[t]) umma_commit(&o_done[t]);
+          if (j + 1 < nk[t]) {
+            if (!k_ready) { wait_k(j + 1); k_ready = true; }
+            issue_s(t, j + 1);
+          }
+        }
+        umma_commit(&v_empty[v]);
+        if (j + 1 < nkv) {
+          if (!k_ready) wait_k(j + 1);  // a K tile only the other (finished) tile would have used
+          umma_commit(&k_empty[(j + 1) % KST]);
+        }
+      }
+    }
+  } else if (warp >= 4) {  // ---- softmax: tile t, thread <-> row
+    const int t = (warp - 4) >> 2;
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int r = q * 32 + lane;
+    const int n_t = t ? nk[1] : nk[0];
+    const int row_start = t ? tl[1].x : tl[0].x;
+    const int n_rows = t ? tl[1].y : tl[0].y;
+    const int tt = r / G, g = r % G;
+    const bool valid = (r < TQ * G) && (tt < n_rows);
+    const int p = valid ? a.qpos[row_start + tt] : -1;
+    const int p_first = n_t > 0 ? a.qpos[row_start] : 0;  // smallest position of the tile
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t s_col = tmem + lane_base + t * 128;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_t; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      const bool full = j * BKV + BKV - 1 <= p_first;  // every row sees every key: no causal mask
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t sr[64];
+        tmem_ld32(s_col + hh * 64, sr);
+        tmem_ld32(s_col + hh * 64 + 32, sr + 32);
+        tmem_wait_ld();
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (full) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sr[c]));
+        } else {
+          const int key0 = j * BKV + hh * 64;
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            const float v = (key0 + c <= p) ? __uint_as_float(sr[c]) : -INFINITY;
+            sr[c] = __float_as_uint(v);
+            mx4[c & 3] = fmaxf(mx4[c & 3], v);
+          }
+        }
+        // raw scores; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
+        float alpha = 1.f;
+        bool need = false;
+        if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
+          const float m_new = fmaxf(m_run, mx);
+          if (m_run != -INFINITY) { alpha = fast_exp2(m_run - m_new); need = true; }
+          m_run = m_new;
+        }
+        if (__any_sync(0xffffffffu, need)) {  // rare: rebase O_t (PVs up to j-1) and this tile's first-half P
+          if (j > 0) {  // the commit of S_t(j) covered PV_t(j-1): O_t is complete up to j-1
+            uint32_t o[32];
+#pragma unroll 1
+            for (int c = 0; c < DH; c += 32) {
+              tmem_ld32(tmem + lane_base + O_COL + t * 128 + c, o);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st32(tmem + lane_base + O_COL + t * 128 + c, o);
+            }
+          }
+          if (hh == 1) {
+            uint32_t pp[32];
+            tmem_wait_st();
+            tmem_ld32(s_col, pp);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              pp[i] = pack_bf2(__uint_as_float(pp[i] << 16) * alpha, __uint_as_float(pp[i] & 0xFFFF0000u) * alpha);
+            tmem_st32(s_col, pp);
+          }
+          tmem_wait_st();
+        }
+        l_run *= alpha;
+        const float base = (m_run == -INFINITY) ? 0.f : m_run;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 64; c += 8) {
+          float e[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float x = fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base);
+            // one chunk in four on the FMA pipe: the SFU (16 ex2/clk/SM) is the co-bottleneck
+            e[i] = ((c >> 3) % 4 == 3) ? poly_exp2(x) : fast_exp2(x);
+            ls[i & 3] += e[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf2(e[2 * i], e[2 * i + 1]);
+        }
+        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    if (n_t > 0) {
+      mbar_wait(&o_done[t], 0);
+      tc_fence_after();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      uint16_t* dst = a.o + static_cast<int64_t>(row_start + tt) * H * DH + (kvh * G + g) * DH;
+#pragma unroll 1
+      for (int c = 0; c < DH; c += 32) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_base + O_COL + t * 128 + c, o);
+        tmem_wait_ld();
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 u;
+            u.x = pack_bf2(__uint_as_float(o[i + 0]) * inv, __uint_as_float(o[i + 1]) * inv);
+            u.y = pack_bf2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+            u.z = pack_bf2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+            u.w = pack_bf2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c + i) = u;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+}  // namespace
+
+cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                             const AttnArgs& a, int64_t t_cap, cudaStream_t s) {
+  if (a.n_tiles <= 0) return cudaSuccess;
+  if (a.n_tiles % 2 != 0 || a.head_dim != DH || a.n_splits != 1) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_attn_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_pdl(k_attn_pair, dim3(a.n_tiles / 2, a.n_kv_heads), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV,
+                    a, t_cap);
+}
+
+bool attn_use_pairs(int n_tiles, int n_kv_heads, int num_sms) {
+  static const int forced = [] {
+    const char* e = getenv("RC_ATTN_PAIRS");  // diagnostics: 0 = never, 1 = always
+    return e ? atoi(e) : -1;
+  }();
+  if (forced == 0 || forced == 1) return forced == 1;
+  // pairs halve the CTA count: only when at least 4 waves of paired CTAs remain
+  return static_cast<int64_t>(n_tiles) * n_kv_heads >= static_cast<int64_t>(8) * num_sms;
+}
+
+}  // namespace rc

@@ -776,8 +776,8 @@ rc_status rc_sel_count(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_pr
 namespace {
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
 rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
-                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, double attn_flops,
-                    int attn_pending, cudaStream_t s) {
+                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, bool paired,
+                    double attn_flops, int attn_pending, cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
   const double R = rows, norm_b = R * d * 6.0;
@@ -815,7 +815,10 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
     at.part_ml = c->part_ml;
     c->launches += 1;  // the merge kernel
   }
-  if (c->attn_tc)
+  if (paired)
+    RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
+              attn_pair_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
+  else if (c->attn_tc)
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
               attn_tc_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
   else
@@ -877,13 +880,32 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   for (auto& p : plan) { n_ut += ntiles(p.u_cnt); n_st += ntiles(p.sel_cnt); }
   // small grids (e.g. one request's selected rows) fill the SMs badly: split the KV range of every
   // query tile over several CTAs and merge (tcgen05 kernel only); every entry repeats per split
+  if (prm->attn_kernel < RC_ATTN_AUTO || prm->attn_kernel > RC_ATTN_SPLIT2)
+    return fail(RC_E_INVALID, "attn_kernel must be one of RC_ATTN_*");
+  const int ak = c->attn_tc ? prm->attn_kernel : RC_ATTN_SINGLE;
   int split_u = 1, split_s = 1;
-  if (c->attn_tc) {
+  if (ak == RC_ATTN_SPLIT2) {
+    split_u = split_s = 2;
+  } else if (ak == RC_ATTN_AUTO && c->attn_tc) {
     int64_t ntok = 0;
     for (auto& p : plan) ntok += p.sq->n;
     const int est_kv = static_cast<int>(ntok / n_req / 128) + 1;
     split_u = attn_tc_choose_splits(n_ut, m.n_kv_heads, est_kv, c->num_sms);
     split_s = attn_tc_choose_splits(n_st, m.n_kv_heads, est_kv, c->num_sms);
+  }
+  // large grids: two query tiles of one request per CTA share every K/V tile load (k_attn_pair.cu);
+  // a request's odd tile count is padded with one empty tile
+  bool pair_u = false, pair_s = false;
+  if (c->attn_tc && m.head_dim == 128 && (ak == RC_ATTN_AUTO || ak == RC_ATTN_PAIRED)) {
+    pair_u = split_u == 1 && (ak == RC_ATTN_PAIRED || attn_use_pairs(n_ut, m.n_kv_heads, c->num_sms));
+    pair_s = split_s == 1 && (ak == RC_ATTN_PAIRED || attn_use_pairs(n_st, m.n_kv_heads, c->num_sms));
+    auto padded = [&](bool u) {
+      int32_t n = 0;
+      for (auto& p : plan) n += (ntiles(u ? p.u_cnt : p.sel_cnt) + 1) / 2 * 2;
+      return n;
+    };
+    if (pair_u) n_ut = padded(true);
+    if (pair_s) n_st = padded(false);
   }
   n_ut *= split_u;
   n_st *= split_s;
@@ -918,8 +940,10 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     const int arow = static_cast<int>(sq.arena_row);
     for (int i = 0; i < p.u_cnt; i += TQ)
       for (int sp = 0; sp < split_u; ++sp) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), arow, sp);
+    if (pair_u && ntiles(p.u_cnt) % 2) hut[iu++] = make_int4(p.u_off + p.u_cnt, 0, arow, 0);
     for (int i = 0; i < p.sel_cnt; i += TQ)
       for (int sp = 0; sp < split_s; ++sp) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), arow, sp);
+    if (pair_s && ntiles(p.sel_cnt) % 2) hst[is++] = make_int4(p.sel_off + p.sel_cnt, 0, arow, 0);
     H32(o_last)[r] = p.sel_off + p.sel_cnt - 1;
     for (size_t j = 0; j < sq.cand_idtok.size(); ++j) { H32(o_creq)[ic] = r; H32(o_cid)[ic] = sq.cand_idtok[j]; ++ic; }
     if (forced) {
@@ -946,7 +970,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   attn_u *= 4.0 * m.n_heads * m.head_dim;
   const int pend_idx = c->prof ? static_cast<int>(c->pend.size()) : -1;
   for (int l = 0; l < cL; ++l) {
-    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, attn_u, -1, s);
+    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, pair_u, attn_u, -1, s);
     if (st != RC_OK) return st;
   }
   // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
@@ -982,7 +1006,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
             gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
   // ---- a5-a7: selective layers c..L-1 on Sel
   for (int l = cL; l < L; ++l) {
-    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, 0.0, pend_idx, s);
+    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, pair_s, 0.0, pend_idx, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout

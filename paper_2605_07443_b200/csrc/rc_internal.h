@@ -110,6 +110,11 @@ int attn_tc_tokens_per_tile(int group);
 int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms);
 cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV, const AttnArgs& a,
                            int64_t t_cap, cudaStream_t s);
+// paired-tile version for large grids (k_attn_pair.cu): a.tiles holds 2 entries per CTA, both of one
+// request (odd counts padded with an empty tile); n_splits must be 1
+cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV,
+                             const AttnArgs& a, int64_t t_cap, cudaStream_t s);
+bool attn_use_pairs(int n_tiles, int n_kv_heads, int num_sms);
 bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
                        uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 

@@ -102,7 +102,7 @@ def test_deviation_and_selection_bitexact(n_u, width, r_bp, window):
 
 
 # ----------------------------------------------------------------------------- end to end
-def _run_gpu(wl, case, pools, r_bp, c=1, forced=None, no_prefix=False, hidden=True, window=0):
+def _run_gpu(wl, case, pools, r_bp, c=1, forced=None, no_prefix=False, hidden=True, window=0, attn_kernel=0):
     G = _gpu()
     n_tok = sum(l.n for l in layouts(case))
     ctx, _ = G.make_ctx(case, pools, n_tok)
@@ -113,7 +113,7 @@ def _run_gpu(wl, case, pools, r_bp, c=1, forced=None, no_prefix=False, hidden=Tr
     seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=c)
     n_cand = sum(len(l["cand_idtok"]) for l in lays)
     out = ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, window=window, forced_sel=forced, hidden=hidden,
-                                n_cand=n_cand)
+                                n_cand=n_cand, attn_kernel=attn_kernel)
     torch.cuda.synchronize()
     res = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
     res["kv_last"] = [tuple(G.bits(t) for t in ctx.read_kv(s, wl.shape.n_layers - 1, lay["tokens"].shape[0]))
@@ -185,5 +185,25 @@ def test_ragged_batch_matches_per_request():
     for r, lay in enumerate(layouts(case)):
         sel = res["sel_pos"][off[r]:off[r + 1]]
         forced, _ = _oracle_forced(case, pools, lay, sel, 1500)
+        assert rel_l2(res["logits"][r], forced["logits"]) < TOL
+        assert rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
+
+
+@pytest.mark.parametrize("wl", [rcgen.MINI_L, rcgen.MINI_Q])
+@pytest.mark.parametrize("attn_kernel", [1, 2, 3])
+def test_attention_launch_shapes_match_oracle(wl, attn_kernel):
+    """Every attention launch shape (one query tile per CTA, two tiles of one request per CTA with
+    an odd tile count padded, KV split + merge) on a ragged 3-request batch, layers < c included."""
+    from paper_2605_07443_b200 import _lib as R
+    assert (R.RC_ATTN_SINGLE, R.RC_ATTN_PAIRED, R.RC_ATTN_SPLIT2) == (1, 2, 3)
+    case = make_case(wl, n_req=3)
+    pools = oracle_pools(case)
+    res, lays = _run_gpu(wl, case, pools, 1500, attn_kernel=attn_kernel)
+    off = res["sel_off"]
+    for r, lay in enumerate(layouts(case)):
+        sel = res["sel_pos"][off[r]:off[r + 1]]
+        forced, own = _oracle_forced(case, pools, lay, sel, 1500)
+        jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
+        assert jac >= 0.8, jac
         assert rel_l2(res["logits"][r], forced["logits"]) < TOL
         assert rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
