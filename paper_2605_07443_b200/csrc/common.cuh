@@ -269,4 +269,91 @@ __device__ __forceinline__ float poly_exp2(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
+// ---- packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes' worth per instruction)
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// ---- one 64-key step of an online softmax row (attention kernels; thread <-> query row)
+// Row maximum of 64 raw scores; MASKED: keys key0 + c > p are excluded (causal by true position).
+template <bool MASKED>
+__device__ __forceinline__ float sm_rowmax64(const uint32_t* sr, int key0, int p) {
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    float v = __uint_as_float(sr[c]);
+    if (MASKED) v = (key0 + c <= p) ? v : -INFINITY;
+    m4[c & 3] = fmaxf(m4[c & 3], v);
+  }
+  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+}
+
+// P = 2^(s * scale - base) for 64 raw scores, packed as bf16 pairs into pk[32]; returns the sum of
+// the fp32 values. Arithmetic on fp32x2 pairs; 3 chunks of 8 keys in 8 take 2^x on the FMA pipe
+// (poly_exp2 written out on pairs), the rest on the SFU (16 ex2/clk/SM), balancing the two pipes.
+template <bool MASKED>
+__device__ __forceinline__ float sm_exp_pack64(const uint32_t* sr, uint32_t* pk, int key0, int p, float scale,
+                                               float base) {
+  const uint64_t sc2 = f2_pack(scale, scale), nb2 = f2_pack(-base, -base);
+  const uint64_t mg2 = f2_pack(12582912.f, 12582912.f);
+  const uint64_t c3 = f2_pack(0.0555041086648216f, 0.0555041086648216f);
+  const uint64_t c2 = f2_pack(0.2402265069591007f, 0.2402265069591007f);
+  const uint64_t c1 = f2_pack(0.6931471805599453f, 0.6931471805599453f);
+  const uint64_t c0 = f2_pack(1.f, 1.f);
+  uint64_t acc[2] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < 64; c += 2) {
+    const uint64_t x2 = f2_fma(f2_pack(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), sc2, nb2);
+    float x0, x1, e0, e1;
+    f2_unpack(x2, x0, x1);
+    if (MASKED) {
+      x0 = (key0 + c <= p) ? x0 : -INFINITY;
+      x1 = (key0 + c + 1 <= p) ? x1 : -INFINITY;
+    }
+    const int chunk = c >> 3;
+    if (chunk == 2 || chunk == 5 || chunk == 7) {
+      const uint64_t xc = f2_pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+      const uint64_t t2 = f2_add(xc, mg2);
+      const uint64_t f = f2_sub(xc, f2_sub(t2, mg2));
+      uint64_t pp = f2_fma(f, c3, c2);
+      pp = f2_fma(pp, f, c1);
+      pp = f2_fma(pp, f, c0);
+      float p0, p1, t0, t1;
+      f2_unpack(pp, p0, p1);
+      f2_unpack(t2, t0, t1);
+      e0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+      e1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+    } else {
+      e0 = fast_exp2(x0);
+      e1 = fast_exp2(x1);
+    }
+    acc[(c >> 1) & 1] = f2_add(acc[(c >> 1) & 1], f2_pack(e0, e1));
+    pk[c >> 1] = pack_bf2(e0, e1);
+  }
+  float a0, a1, b0, b1;
+  f2_unpack(acc[0], a0, a1);
+  f2_unpack(acc[1], b0, b1);
+  return (a0 + a1) + (b0 + b1);
+}
+
 }  // namespace rc

@@ -60,7 +60,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(q_full, 1);
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    for (int t = 0; t < 2; ++t) { mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 128); mbar_init(&o_done[t], 1); }
+    // p_full: one arrival per softmax warp (lane 0 after __syncwarp), not per thread
+    for (int t = 0; t < 2; ++t) { mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 4); mbar_init(&o_done[t], 1); }
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -127,10 +128,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(&k_full[j % KST], (j / KST) & 1);
         tc_fence_after();
       };
+      const bool no_mma = (a.debug_mode & 2) != 0;  // diagnostics: barriers only
       auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
         const int s = j % KST;
 #pragma unroll
-        for (int k = 0; k < DH / 16; ++k) {
+        for (int k = 0; k < (no_mma ? 0 : DH / 16); ++k) {
           const uint64_t ad = sdesc_sw128(smem_u32(sQ + t * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
           const uint64_t bd = sdesc_sw128(smem_u32(sK + s * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
           umma_bf16(tmem + t * 128, ad, bd, idS, k > 0);
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&p_full[t], j & 1);
           tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < BKV / 16; ++k) {  // 16 keys per MMA: A = P_t (8 TMEM columns), B = V rows
+          for (int k = 0; k < (no_mma ? 0 : BKV / 16); ++k) {  // 16 keys per MMA: A = P_t (8 TMEM columns), B = V rows
             const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + v * TILE + k * 2048), HALF, 1024);
             umma_bf16_ts(tmem + O_COL + t * 128, tmem + t * 128 + k * 8, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
           }
@@ -187,28 +189,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int j = 0; j < n_t; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const bool full = j * BKV + BKV - 1 <= p_first;  // every row sees every key: no causal mask
+      if (a.debug_mode & 1) {  // diagnostics: no softmax work
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+        continue;
+      }
 #pragma unroll 1
       for (int hh = 0; hh < 2; ++hh) {
         uint32_t sr[64];
         tmem_ld32(s_col + hh * 64, sr);
         tmem_ld32(s_col + hh * 64 + 32, sr + 32);
         tmem_wait_ld();
-        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        if (full) {
-#pragma unroll
-          for (int c = 0; c < 64; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sr[c]));
-        } else {
-          const int key0 = j * BKV + hh * 64;
-#pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            const float v = (key0 + c <= p) ? __uint_as_float(sr[c]) : -INFINITY;
-            sr[c] = __float_as_uint(v);
-            mx4[c & 3] = fmaxf(mx4[c & 3], v);
-          }
-        }
+        const int key0 = j * BKV + hh * 64;
+        const bool full = key0 + 63 <= p_first;  // every row sees every key of the half: no causal mask
+        const float rmax = full ? sm_rowmax64<false>(sr, key0, p) : sm_rowmax64<true>(sr, key0, p);
         // raw scores; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
-        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
+        const float mx = rmax * a.scale_log2;
         float alpha = 1.f;
         bool need = false;
         if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
@@ -242,27 +238,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         l_run *= alpha;
         const float base = (m_run == -INFINITY) ? 0.f : m_run;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[32];
-#pragma unroll
-        for (int c = 0; c < 64; c += 8) {
-          float e[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float x = fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base);
-            // one chunk in four on the FMA pipe: the SFU (16 ex2/clk/SM) is the co-bottleneck
-            e[i] = ((c >> 3) % 4 == 3) ? poly_exp2(x) : fast_exp2(x);
-            ls[i & 3] += e[i];
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf2(e[2 * i], e[2 * i + 1]);
-        }
-        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
+                      : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
         tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
     if (n_t > 0) {
       mbar_wait(&o_done[t], 0);

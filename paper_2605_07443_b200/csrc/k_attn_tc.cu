@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
     for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 4; ++i) { mbar_init(&p_full[i], 128); mbar_init(&pv_done[i], 1); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&p_full[i], 4); mbar_init(&pv_done[i], 1); }  // p_full: 1 per warp
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -172,20 +172,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_ld32(tmem + lane_base + b * 128 + col0 + 32, sr + 32);
       tmem_wait_ld();
       const int key0 = (j0 + j) * BKV + col0;
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
-      if ((j0 + j) * BKV + BKV - 1 <= p_first) {  // every row of the tile sees every key: no causal mask
-#pragma unroll
-        for (int c = 0; c < SCOLS; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], __uint_as_float(sr[c]));
-      } else {
-#pragma unroll
-        for (int c = 0; c < SCOLS; ++c) {
-          const float v = (key0 + c <= p) ? __uint_as_float(sr[c]) : -INFINITY;
-          sr[c] = __float_as_uint(v);
-          mx4[c & 3] = fmaxf(mx4[c & 3], v);
-        }
-      }
+      const bool full = key0 + SCOLS - 1 <= p_first;  // every row sees every key of the half: no mask
       // scores stay raw; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * a.scale_log2;
+      const float mx = (full ? sm_rowmax64<false>(sr, key0, p) : sm_rowmax64<true>(sr, key0, p)) * a.scale_log2;
       float alpha = 1.f;
       bool need = false;
       if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
@@ -210,26 +199,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       l_run *= alpha;
       const float base = (m_run == -INFINITY) ? 0.f : m_run;
       // P (bf16 pairs) overwrites the first 32 of this group's own 64 S columns (already in registers)
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[SCOLS / 2];
-#pragma unroll
-      for (int c = 0; c < SCOLS; c += 8) {
-        float e[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float x = fmaf(__uint_as_float(sr[c + i]), a.scale_log2, -base);
-          // one chunk in four on the FMA pipe: the SFU (16 ex2/clk/SM) is the co-bottleneck
-          e[i] = ((c >> 3) % 4 == 3) ? poly_exp2(x) : fast_exp2(x);
-          ls[i & 3] += e[i];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) pk[c / 2 + i] = pack_bf2(e[2 * i], e[2 * i + 1]);
-      }
-      l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
+                    : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
       tmem_st32(tmem + lane_base + b * 128 + col0, pk);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[b * 2 + h]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b * 2 + h]);
     }
     // merge the two halves: O = (O_0 2^(m_0-m) + O_1 2^(m_1-m)) / (l_0 2^(m_0-m) + l_1 2^(m_1-m))
     red[(h * 2 + 0) * 128 + r] = m_run;
