@@ -28,6 +28,46 @@ def importance_scores(A, K_new, K_cached, V_new, V_cached, lam):
     return (1.0 - lam) * A + lam * div
 
 
+MASS_FRAC_BITS = 24  # fixed point of the attention mass (NEXT-1 reading R2-FX)
+
+
+def attention_mass_fixed(q, qpos, K, n_heads, n_kv_heads, head_dim):
+    """||A_p||_1 of Eq. 3 as the column mass of the check-layer softmax (reading R2):
+    A[p] = sum over heads h and queries q with pos_q >= p of P[h, q, p], P the causal softmax of
+    q_h . K_{g(h)} / sqrt(d_h) over all keys at positions <= pos_q, g(h) = floor(h / (H / H_kv)).
+    Fixed point (reading R2-FX): every term enters as floor(P * 2^24), summed exactly as integers.
+    q: [T][H][dh] fp64 (fresh queries at layer c), qpos: [T], K: [n][Hk][dh] fp64 keys by position.
+    Returns uint64 [n]."""
+    q = np.asarray(q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    qpos = np.asarray(qpos, dtype=np.int64)
+    n = K.shape[0]
+    G = n_heads // n_kv_heads
+    scale = 1.0 / np.sqrt(head_dim)
+    kpos = np.arange(n)
+    A = np.zeros(n, dtype=np.uint64)
+    for t0 in range(0, len(qpos), 512):
+        t1 = min(len(qpos), t0 + 512)
+        mask = kpos[None, :] > qpos[t0:t1, None]
+        for h in range(n_heads):
+            sc = (q[t0:t1, h] @ K[:, h // G].T) * scale
+            sc = np.where(mask, -np.inf, sc)
+            sc = sc - sc.max(axis=1, keepdims=True)
+            p = np.exp(sc)
+            p /= p.sum(axis=1, keepdims=True)
+            A += np.floor(p * float(1 << MASS_FRAC_BITS)).astype(np.uint64).sum(axis=0)
+    return A
+
+
+def combine_fixed(A_fx, D_fx, lam):
+    """Eq. 3 on the fixed-point terms: S = rint((1 - lam) * A + lam * D) in IEEE fp64, round half to
+    even (reading R2-FX: A and D both carry 24 fraction bits, so S does too). uint64 [n]."""
+    A = np.asarray(A_fx, dtype=np.uint64).astype(np.float64)
+    D = np.asarray(D_fx, dtype=np.uint64).astype(np.float64)
+    lam = float(lam)
+    return np.rint((1.0 - lam) * A + lam * D).astype(np.uint64)
+
+
 def topk_order(scores, idx):
     """Indices `idx` sorted by (score desc, index asc) -- the R6 order."""
     return sorted((int(i) for i in idx), key=lambda i: (-scores[i], i))

@@ -6,8 +6,11 @@ positions and c the check layer (reading R1):
   2. Layers l < c: the full layer for every p in U over prefix + U, causal ("full attention
      computation in the first decoder layer"); KV_st[l][U] := fresh.
   3. Check layer c: K_new, V_new for U (RoPE at p); for HIST/ITEM tokens the Eq. 3 divergence
-     with lambda = 1 (R3) in the R4 fixed point, on K_new/V_new rounded to the bf16 value they
-     would be stored as vs the stitched bf16 value.
+     in the R4 fixed point, on K_new/V_new rounded to the bf16 value they would be stored as vs
+     the stitched bf16 value. lambda = 1 (R3) scores by D alone; lambda < 1 (NEXT-1) adds the
+     attention-mass term: the fresh queries of U attend, causally, over the fresh keys (prefix
+     cache + K_new of U) -- "full attention computation in the first decoder layer"
+      -- and S = (1 - lambda) A + lambda D (Eq. 3) in the R2-FX fixed point.
   4. Sel = FORCED u window u topk per class (select.select_sel; R5-R7), or a forced Sel.
   5. Layers c..L-1 on Sel only: q, k, v at the true positions, KV_st[l][Sel] := (k, v),
      non-selected tokens keep their stitched state (R9), attention of every selected query
@@ -19,11 +22,11 @@ import numpy as np
 
 from .layout import PREFIX, HIST, ITEM
 from .numerics import bf16_to_f32, round_bf16, deviation_fixed
-from .select import select_sel
+from .select import select_sel, attention_mass_fixed, combine_fixed
 
 
 def selective_prefill(m, layout, K_bits, V_bits, r_rev_bp, r_item_bp, check_layer=1,
-                      window=0, forced_sel=None, keep_kv=True, exact_kv=False):
+                      window=0, forced_sel=None, keep_kv=True, exact_kv=False, lam=1.0):
     """K_bits, V_bits: stitched cache per layer [n][Hk][dh] as bf16 bit patterns (O-ASM), or
     fp64 values when exact_kv (lossless test mode of the exact-cache invariant)."""
     s = m.s
@@ -45,8 +48,8 @@ def selective_prefill(m, layout, K_bits, V_bits, r_rev_bp, r_item_bp, check_laye
         o = m.attend(q, U, K[l], V[l])
         x = m.post(l, x, o)
 
-    # check layer c: deviation of the fresh K/V from the stitched cache (lambda = 1)
-    _, k_new, v_new = m.qkv(c, x, U)
+    # check layer c: deviation of the fresh K/V from the stitched cache
+    q_new, k_new, v_new = m.qkv(c, x, U)
     D = np.zeros(n, dtype=np.uint64)
     reuse = np.array([cls[p] in (HIST, ITEM) for p in U])
     if reuse.any():
@@ -55,8 +58,17 @@ def selective_prefill(m, layout, K_bits, V_bits, r_rev_bp, r_item_bp, check_laye
         vb = round_bf16(v_new[reuse]).reshape(len(ur), -1)
         D[ur] = deviation_fixed(kb, round_bf16(K[c][ur]).reshape(len(ur), -1)) + \
             deviation_fixed(vb, round_bf16(V[c][ur]).reshape(len(ur), -1))
+    A = None
+    S = D
+    if lam < 1.0:  # NEXT-1: attention mass of the fresh layer-c softmax (prefix keys are exact)
+        K_fresh = K[c].copy()
+        K_fresh[U] = k_new
+        A = attention_mass_fixed(q_new, U, K_fresh, s.n_heads, s.n_kv_heads, s.head_dim)
+        S = np.zeros(n, dtype=np.uint64)
+        ru = U[reuse] if len(U) else U
+        S[ru] = combine_fixed(A[ru], D[ru], lam)
     if forced_sel is None:
-        sel = select_sel(cls, D, r_rev_bp, r_item_bp, window)
+        sel = select_sel(cls, S, r_rev_bp, r_item_bp, window)
     else:
         sel = np.array(sorted(int(p) for p in forced_sel), dtype=np.int32)
     row_of = {int(p): i for i, p in enumerate(U)}
@@ -72,7 +84,7 @@ def selective_prefill(m, layout, K_bits, V_bits, r_rev_bp, r_item_bp, check_laye
     cand = logits[layout.cand_idtok.astype(np.int64)]
     rank = sorted(range(len(cand)), key=lambda i: (-cand[i], i))
     out = {"logits": logits, "cand_scores": cand, "rank": np.array(rank), "sel": sel,
-           "D": D, "x_sel": xs}
+           "D": D, "A": A, "S": S, "x_sel": xs}
     if keep_kv:
         out["K"], out["V"] = K, V
     return out

@@ -163,8 +163,9 @@ def test_selective_r0_equals_hf_tail_over_stitched_cache(c):
         assert np.array_equal(bf16_bits(sel["K"][l][:n - T].astype(np.float32)), K[l][:n - T])
 
 
-@pytest.mark.parametrize("r_bp,c", [(0, 1), (1500, 1), (1500, 0), (5000, 1)])
-def test_exact_cache_selective_equals_full(r_bp, c):
+@pytest.mark.parametrize("r_bp,c,lam", [(0, 1, 1.0), (1500, 1, 1.0), (1500, 0, 1.0), (5000, 1, 1.0),
+                                        (1500, 0, 0.5), (3000, 1, 0.0)])
+def test_exact_cache_selective_equals_full(r_bp, c, lam):
     # pools holding the O-FULL KV of this very prompt at the same positions (Delta = 0),
     # kept lossless (fp32 test mode): the stitched cache IS the full-prefill cache
     case, m, pools, lay = _tiny_setup(rcgen.CFG1)
@@ -172,12 +173,30 @@ def test_exact_cache_selective_equals_full(r_bp, c):
     full = full_prefill(m, lay.tokens.tolist())
     Kx = [full["K"][l].copy() for l in range(s.n_layers)]
     Vx = [full["V"][l].copy() for l in range(s.n_layers)]
-    sel = selective_prefill(m, lay, Kx, Vx, r_bp, r_bp, check_layer=c, exact_kv=True)
+    sel = selective_prefill(m, lay, Kx, Vx, r_bp, r_bp, check_layer=c, exact_kv=True, lam=lam)
     assert rel_l2(sel["logits"], full["logits_last"]) < 1e-10
     for l in range(s.n_layers):
         assert rel_l2(sel["K"][l], full["K"][l]) < 1e-10
     # deviation: K_new equals the cached K up to bf16 rounding of one side -> D <= 1 ulp terms
     assert int(sel["D"].max()) <= 2 * s.n_kv_heads * s.head_dim * 2 ** 24 // 64
+
+
+def test_selective_lambda_one_is_deviation_only_and_lambda_orders_by_mass():
+    case, m, pools, lay = _tiny_setup(rcgen.CFG1)
+    K, V, _ = assemble(case["shape"], lay, pools["items"], pools["hist"], pools["prefix"], gather_from=1)
+    a = selective_prefill(m, lay, K, V, 1500, 1500, lam=1.0)
+    assert a["A"] is None and np.array_equal(a["S"], a["D"])
+    b = selective_prefill(m, lay, K, V, 1500, 1500, lam=0.0)
+    # lambda = 0: S = A on HIST/ITEM rows, and the budgets pick the largest column masses per class
+    reuse = np.isin(lay.cls, [HIST, ITEM])
+    assert np.array_equal(b["S"][reuse], b["A"][reuse])
+    assert len(b["sel"]) == len(a["sel"])
+    for cl in (HIST, ITEM):
+        members = np.nonzero(lay.cls == cl)[0]
+        chosen = [p for p in b["sel"] if lay.cls[p] == cl]
+        rest = [p for p in members if p not in set(chosen)]
+        if chosen and rest:
+            assert min(int(b["A"][p]) for p in chosen) >= max(int(b["A"][p]) for p in rest)
 
 
 def test_selective_deterministic_and_sel_shape():

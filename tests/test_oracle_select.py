@@ -96,3 +96,79 @@ def test_importance_scores_reductions_and_brute_force():
         assert abs(S[i] - t) < 1e-12
     with pytest.raises(ValueError):
         importance_scores(A[:-1], Kn, Kc, Vn, Vc, 0.5)
+
+
+# ----------------------------------------------------------------------------- NEXT-1: attention mass
+from oracle.select import attention_mass_fixed, combine_fixed, MASS_FRAC_BITS  # noqa: E402
+
+ONE = 1 << MASS_FRAC_BITS
+
+
+def _mass_case(seed, n=40, P=8, H=4, Hk=2, dh=16):
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((n - P, H, dh)) * 2.0
+    K = rng.standard_normal((n, Hk, dh))
+    return q, np.arange(P, n), K
+
+
+def test_attention_mass_rows_sum_to_one():
+    """Every softmax row sums to 1 over its keys: sum_p A[p] = H |U| 2^24 minus the floor losses."""
+    q, qpos, K = _mass_case(1)
+    H = q.shape[1]
+    A = attention_mass_fixed(q, qpos, K, H, K.shape[1], q.shape[2])
+    total = int(A.sum())
+    terms = H * int(sum(p + 1 for p in qpos))
+    assert H * len(qpos) * ONE - terms <= total <= H * len(qpos) * ONE
+    assert A[qpos[-1] + 1:].sum() == 0 if qpos[-1] + 1 < len(A) else True
+
+
+def test_attention_mass_uniform_closed_form():
+    """q = 0: every visible key gets 1/(pos_q + 1), so A[p] = H * sum_{pos_q >= p} floor(2^24 / (pos_q + 1))."""
+    _, qpos, K = _mass_case(2)
+    H = 4
+    q = np.zeros((len(qpos), H, K.shape[2]))
+    A = attention_mass_fixed(q, qpos, K, H, K.shape[1], K.shape[2])
+    ref = [H * sum(ONE // (int(t) + 1) for t in qpos if t >= p) for p in range(K.shape[0])]
+    assert [int(a) for a in A] == ref
+
+
+def test_attention_mass_gqa_grouping():
+    """Heads h use kv head floor(h / G): zero keys in kv head 1 make heads 2, 3 uniform, heads 0, 1 equal
+    the single-kv-head computation on kv head 0 (a wrong h -> kv map fails this)."""
+    q, qpos, K = _mass_case(3)
+    K[:, 1] = 0.0
+    A = attention_mass_fixed(q, qpos, K, 4, 2, K.shape[2])
+    A01 = attention_mass_fixed(q[:, :2], qpos, K[:, :1], 2, 1, K.shape[2])
+    unif = np.array([2 * sum(ONE // (int(t) + 1) for t in qpos if t >= p) for p in range(K.shape[0])], np.uint64)
+    assert np.array_equal(A, A01 + unif)
+
+
+def test_attention_mass_brute_force_tiny():
+    """Independent scalar evaluation with math.exp / math.fsum on a 7-token instance."""
+    import math
+    rng = np.random.default_rng(4)
+    n, P, H, Hk, dh = 7, 2, 2, 1, 4
+    q = rng.standard_normal((n - P, H, dh))
+    K = rng.standard_normal((n, Hk, dh))
+    qpos = list(range(P, n))
+    ref = [0] * n
+    for h in range(H):
+        for i, t in enumerate(qpos):
+            sc = [math.fsum(q[i, h, d] * K[p, 0, d] for d in range(dh)) / math.sqrt(dh) for p in range(t + 1)]
+            mx = max(sc)
+            e = [math.exp(x - mx) for x in sc]
+            z = math.fsum(e)
+            for p in range(t + 1):
+                ref[p] += math.floor(e[p] / z * ONE)
+    A = attention_mass_fixed(q, qpos, K, H, Hk, dh)
+    assert [int(a) for a in A] == ref
+
+
+def test_combine_fixed_reductions_and_rounding():
+    A = np.array([3, 1, 0, 7, 2 ** 40], np.uint64)
+    D = np.array([4, 4, 9, 7, 2 ** 50], np.uint64)
+    assert np.array_equal(combine_fixed(A, D, 1.0), D)
+    assert np.array_equal(combine_fixed(A, D, 0.0), A)
+    # 3.5 -> 4, 2.5 -> 2 (half to even), 4.5 -> 4, 7 -> 7
+    assert combine_fixed(A, D, 0.5)[:4].tolist() == [4, 2, 4, 7]
+    assert int(combine_fixed(A, D, 0.5)[4]) == (2 ** 40 + 2 ** 50) // 2
