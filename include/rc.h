@@ -39,7 +39,7 @@ typedef int32_t rc_status;
 #define RC_E_EXISTS (-5)      /* duplicate block id on registration                         */
 #define RC_E_CUDA (-6)        /* CUDA runtime error (message has the CUDA error string)     */
 #define RC_E_PEER (-7)        /* peer pool not attached / not accessible                    */
-#define RC_E_UNSUPPORTED (-8) /* parameter combination not built yet (e.g. lambda != 1)     */
+#define RC_E_UNSUPPORTED (-8) /* parameter combination not built (lambda < 1 with head_dim != 128) */
 
 typedef struct rc_ctx rc_ctx;
 typedef uint64_t rc_seq;     /* handle of an assembled request (its stitched KV) */
@@ -121,7 +121,9 @@ typedef struct rc_prompt {
 typedef struct rc_prefill_params {
   int32_t r_rev_bp;           /* recompute ratio of history tokens, basis points (R5)        */
   int32_t r_item_bp;          /* recompute ratio of item tokens, basis points; 10000 = all   */
-  float lambda;               /* Eq. 3 lambda; must be 1.0 (deviation-only, R3)              */
+  float lambda;               /* Eq. 3 lambda in [0, 1]: 1 = deviation only (R3, default);
+                                 < 1 adds the attention-mass term (NEXT-1, R2 / R2-FX):
+                                 S = rint((1 - lambda) A + lambda D) in fp64 from this fp32 */
   int32_t check_layer;        /* c: layers < c full over U, deviation at c (R1), 0 <= c < L   */
   int32_t window;             /* last `window` positions always recomputed (R7)              */
   const int32_t* forced_sel;  /* optional host list: Sel positions per request, concatenated,
@@ -130,6 +132,9 @@ typedef struct rc_prefill_params {
   int32_t attn_kernel;        /* attention launch shape (d_h = 128): RC_ATTN_AUTO chooses by grid
                                  size; the others force one (tests). Results agree within the
                                  rounding of the online softmax, not bit for bit */
+  uint64_t* score_out;        /* optional device [sum of |U| over the batch], U rows request-major:
+                                 the selection score of every U row (Eq. 3 fixed point, DESIGN.md
+                                 R4 / R2-FX; only HIST/ITEM rows are meaningful); NULL = none */
 } rc_prefill_params;
 enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3 };
 
@@ -179,8 +184,10 @@ rc_status rc_sel_count(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_
                        int32_t* counts);
 
 /* Selective recomputation over a ragged batch:
- * layers < c over all non-prefix tokens U; Eq. 3 deviation (lambda = 1) at layer c in the R4
- * fixed point; per-class top-k heavy hitters (R5/R6) + FORCED + window; layers c..L-1 for the
+ * layers < c over all non-prefix tokens U; Eq. 3 at layer c: the deviation D in the R4 fixed
+ * point and, for lambda < 1, the attention mass A of the layer-c softmax of U over the fresh
+ * keys (two extra passes: row log-sum-exp, then column sums, R2-FX);
+ * per-class top-k heavy hitters (R5/R6) + FORCED + window; layers c..L-1 for the
  * selected tokens only over the whole stitched KV (causal by position, R11), updating the
  * stitched KV at Sel; LM head on the last position. r_bp = 10000 with no PREFIX is full
  * prefill. Outputs (DEVICE, caller-allocated, each may be NULL):
@@ -189,7 +196,8 @@ rc_status rc_sel_count(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_
  *   sel_pos     i32 [sum |Sel|]             selected positions, ascending per request
  *   hidden      f32 [sum |Sel|][d]          x_L at Sel (before the final norm, R20)
  * Errors: INVALID (params, c < gather_from of a sequence, forced_sel malformed),
- * UNSUPPORTED (lambda != 1), CAPACITY (sum n > max_batch_tokens), NOTFOUND (seq). */
+ * UNSUPPORTED (lambda < 1 with head_dim != 128), CAPACITY (sum n > max_batch_tokens),
+ * NOMEM (attention-mass workspace on first lambda < 1 call), NOTFOUND (seq). */
 rc_status rc_selective_prefill(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,
                                float* logits, float* cand_scores, int32_t* sel_pos, float* hidden,
                                rc_stream stream);

@@ -61,10 +61,11 @@ def attention_mass_fixed(q, qpos, K, n_heads, n_kv_heads, head_dim):
 
 def combine_fixed(A_fx, D_fx, lam):
     """Eq. 3 on the fixed-point terms: S = rint((1 - lam) * A + lam * D) in IEEE fp64, round half to
-    even (reading R2-FX: A and D both carry 24 fraction bits, so S does too). uint64 [n]."""
+    even (reading R2-FX: A and D both carry 24 fraction bits, so S does too). lam is the fp32
+    parameter of the boundary (rc_prefill_params.lambda) widened to fp64. uint64 [n]."""
     A = np.asarray(A_fx, dtype=np.uint64).astype(np.float64)
     D = np.asarray(D_fx, dtype=np.uint64).astype(np.float64)
-    lam = float(lam)
+    lam = float(np.float32(lam))
     return np.rint((1.0 - lam) * A + lam * D).astype(np.uint64)
 
 

@@ -124,7 +124,7 @@ class RcContext:
         return seqs
 
     def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0, attn_kernel=0):
-        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None, attn_kernel)
+        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None, attn_kernel, None)
         keep = None
         if forced_sel is not None:
             off = np.zeros(len(forced_sel) + 1, np.int32)
@@ -144,11 +144,15 @@ class RcContext:
 
     def selective_prefill(self, seqs, r_rev_bp, r_item_bp, check_layer=1, window=0, forced_sel=None, lam=1.0,
                           logits=True, cand_scores=True, sel_pos=True, hidden=False, n_cand=None, out=None,
-                          stream=None, attn_kernel=0):
+                          stream=None, attn_kernel=0, score_out=None):
         """Returns dict of CUDA tensors (logits, cand_scores, sel_pos, hidden) as requested. `out`
-        may hold preallocated tensors with the same keys (reused; no allocation)."""
+        may hold preallocated tensors with the same keys (reused; no allocation). score_out: optional
+        int64 CUDA tensor [sum |U|] receiving the selection score of every U row (lam < 1: Eq. 3
+        with the attention-mass term, NEXT-1)."""
         seqs = np.ascontiguousarray(seqs, np.uint64)
         prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam, attn_kernel)
+        if score_out is not None:
+            prm.score_out = score_out.data_ptr()
         dev = torch.device("cuda", self.device)
         res = dict(out) if out else {}
         if (sel_pos or hidden) and ("sel_pos" not in res and "hidden" not in res):

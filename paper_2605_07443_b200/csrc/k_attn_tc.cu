@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int G = a.n_heads / a.n_kv_heads;
   const int TQ = ROWS / G;
   const int H = a.n_heads;
-  const int max_pos = a.qpos[row_start + n_rows - 1];
-  const int nkv_all = max_pos / BKV + 1;
+  const int max_pos = n_rows > 0 ? a.qpos[row_start + n_rows - 1] : -1;
+  const int nkv_all = n_rows > 0 ? max_pos / BKV + 1 : 0;  // padded (empty) tiles do nothing
   const int j0 = tile.w * nkv_all / a.n_splits;         // this split's KV tiles [j0, j0 + nkv)
   const int nkv = (tile.w + 1) * nkv_all / a.n_splits - j0;
 
@@ -235,6 +235,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       a.part_ml[prow * 2] = m;
       a.part_ml[prow * 2 + 1] = nkv > 0 ? l_tot : 0.f;
     }
+    if (a.lse_out && h == 0 && valid)  // NEXT-1 pass 1: log2-sum-exp of the scaled scores of this row
+      a.lse_out[static_cast<int64_t>(row_start + t) * H + kvh * G + g] = l_tot > 0.f ? m + __log2f(l_tot) : -INFINITY;
 #pragma unroll
     for (int c = 0; c < 64; c += 32) {
       uint32_t o0[32], o1[32];

@@ -18,7 +18,9 @@ namespace rc {
 
 namespace {
 constexpr int BM = 128, BK = 64;
-constexpr int GROUP_M = 16;  // raster: GROUP_M m-tiles share a sweep over n (L2 reuse of A and B)
+// raster: group_m m-tiles share a sweep over n; the host sizes the group by the bytes of its A rows
+// (they must stay in L2 while the sweep streams B; B is re-read ceil(num_m / group_m) times).
+constexpr size_t GROUP_A_BYTES = size_t(32) << 20;  // measured: gate/up at cfg3 b32 3.14 -> 3.07 ms, DRAM 3.1 -> 1.9 GB vs 16 MB
 
 template <int BN>
 struct GemmCfg {
@@ -81,11 +83,11 @@ __device__ __forceinline__ void epilogue_add_tma(uint32_t taddr, int m0, int n0,
   }
 }
 
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
+  const int per_group = group_m * num_n;
   const int g = t / per_group;
-  const int first_m = g * GROUP_M;
-  const int gm = min(GROUP_M, num_m - first_m);
+  const int first_m = g * group_m;
+  const int gm = min(group_m, num_m - first_m);
   const int r = t - g * per_group;
   mb = first_m + r % gm;
   nb = r / gm;
@@ -256,7 +258,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
 template <int BN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits, const EpiArgs ep) {
+           const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits, int group_m, const EpiArgs ep) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {  // ---------------- TMA producer
       int stage = 0; uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int mb, nb; tile_coords(u / splits, num_m, num_n, mb, nb);
+        int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
         const int sp = u % splits;
         for (int kb = sp * nk / splits; kb < (sp + 1) * nk / splits; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(256, 1)
     int it = 0, chunk_ctr = 0;
     if (EPI == EPI_ADD_F32 && (threadIdx.x & 31) == 0) tma_prefetch_desc(&tmC);
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-      int mb, nb; tile_coords(u / splits, num_m, num_n, mb, nb);
+      int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -384,7 +386,15 @@ cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, const CUtenso
   }
   const int units = tiles * splits;
   const int grid = units < num_sms ? units : num_sms;
-  return launch_pdl(k_gemm<BN, EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits, ep);
+  const int num_m = (M + BM - 1) / BM;
+  static const size_t group_a_bytes = [] {
+    const char* e = std::getenv("RC_GROUP_A_MB");  // diagnostics: L2 budget of the A group
+    return e ? static_cast<size_t>(std::atoi(e)) << 20 : GROUP_A_BYTES;
+  }();
+  const int group_m = static_cast<int>(std::max<size_t>(
+      4, std::min<size_t>(num_m, group_a_bytes / (static_cast<size_t>(BM) * K * 2))));
+  return launch_pdl(k_gemm<BN, EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits, group_m,
+                    ep);
 }
 
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

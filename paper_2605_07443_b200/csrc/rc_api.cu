@@ -221,6 +221,13 @@ struct rc_ctx {
   bool attn_tc = false;                 // tcgen05 attention (head_dim 128)
   CUtensorMap mQ3{};                    // q workspace as [R][H][dh]
   std::vector<CUtensorMap> mK_att, mV_att;  // arena K / V per layer as [Hk*T_cap][dh]
+  // NEXT-1 (lambda < 1): fresh K/V of the check layer (same layout as one arena layer), per-row
+  // log-sum-exp, attention mass; allocated on first use
+  uint16_t* mass_k = nullptr;
+  uint16_t* mass_v = nullptr;
+  float* mass_lse = nullptr;
+  unsigned long long* mass_a = nullptr;
+  CUtensorMap mK_mass{}, mV_mass{};
   int attn_tq() const { return attn_tc ? attn_tc_tokens_per_tile(m.n_heads / m.n_kv_heads)
                                        : attn_tokens_per_tile(m.n_heads / m.n_kv_heads); }
   int bn_qkv = 256, bn_kv = 256, bn_o = 256, bn_d = 256, bn_lm = 256;
@@ -241,7 +248,8 @@ struct rc_ctx {
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
-                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml};
+                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, mass_k, mass_v,
+                    mass_lse, mass_a};
     for (void* p : bufs)
       if (p) cudaFree(p);
   }
@@ -725,7 +733,9 @@ int32_t budget(int32_t r_bp, int32_t count) { return static_cast<int32_t>((stati
 rc_status plan_requests(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,
                         std::vector<ReqPlan>& plan) {
   if (!prm) return fail(RC_E_INVALID, "null params");
-  if (prm->lambda != 1.0f) return fail(RC_E_UNSUPPORTED, "lambda != 1 (attention-mass term, NEXT-1) not built");
+  if (!(prm->lambda >= 0.0f && prm->lambda <= 1.0f)) return fail(RC_E_INVALID, "lambda out of [0, 1]");
+  if (prm->lambda < 1.0f && !c->attn_tc)
+    return fail(RC_E_UNSUPPORTED, "lambda < 1 (attention-mass term) needs the tcgen05 attention (head_dim 128)");
   if (prm->r_rev_bp < 0 || prm->r_rev_bp > 10000 || prm->r_item_bp < 0 || prm->r_item_bp > 10000)
     return fail(RC_E_INVALID, "recompute ratio out of [0, 10000] bp");
   if (prm->check_layer < 0 || prm->check_layer >= c->m.n_layers) return fail(RC_E_INVALID, "check_layer out of range");
@@ -840,6 +850,60 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
 }
 }  // namespace
 
+namespace {
+// NEXT-1 at the check layer c (a = RMSNorm(x_c[U]) already in c->a, D in c->dev): fresh Q/K/V of
+// U into q and the scratch layer, the prefix keys (exact cache) copied next to them, pass 1 (row
+// log-sum-exp over the fresh keys, k_attn_tc), pass 2 (column mass, k_attn_mass), combine into dev.
+rc_status mass_scores(rc_ctx* c, int cL, int32_t U, const int32_t* d_pos, const int32_t* d_dst, const int4* d_ut,
+                      int32_t n_ut, const int4* d_kt, int32_t n_kt, const int4* d_mreq, const std::vector<ReqPlan>& plan,
+                      float lam, cudaStream_t s) {
+  const rc_model_desc& m = c->m;
+  const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads;
+  const int64_t rows = c->pd.arena_rows;
+  cudaError_t e = cudaSuccess;
+  if (!c->mass_k) {
+    const size_t plane = static_cast<size_t>(Hk) * rows * dh;
+    c->mass_k = dev_alloc<uint16_t>(plane, &e);
+    if (e == cudaSuccess) c->mass_v = dev_alloc<uint16_t>(plane, &e);
+    if (e == cudaSuccess) c->mass_lse = dev_alloc<float>(static_cast<size_t>(c->Mx) * H, &e);
+    if (e == cudaSuccess) c->mass_a = dev_alloc<unsigned long long>(c->Mx, &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "attention-mass workspace");
+    if (!make_tmap_bf16_2d(&c->mK_mass, c->mass_k, static_cast<uint64_t>(Hk) * rows, dh, dh, 128) ||
+        !make_tmap_bf16_2d(&c->mV_mass, c->mass_v, static_cast<uint64_t>(Hk) * rows, dh, dh, 128))
+      return fail(RC_E_CUDA, "attention-mass tensor maps");
+  }
+  EpiArgs ep{};
+  ep.bias = c->bqkv ? c->bqkv + static_cast<size_t>(cL) * c->Nqkv : nullptr;
+  ep.pos = d_pos; ep.dst_row = d_dst;
+  ep.q_out = c->q; ep.q_ld = H * dh;
+  ep.arena_k = c->mass_k; ep.arena_v = c->mass_v;
+  ep.head_stride = rows * dh;
+  ep.rope_cos = c->rope_cos; ep.rope_sin = c->rope_sin; ep.rope_zero = c->rope_zero;
+  ep.n_heads = H; ep.n_kv_heads = Hk; ep.head_dim = dh;
+  RC_LAUNCH(RC_K_GEMM, gemm_flops(U, c->Nqkv, d), gemm_bytes(U, c->Nqkv, d, 2), -1,
+            gemm_launch(&c->mA_a, &c->mB_qkv[cL], nullptr, U, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s));
+  for (auto& p : plan)  // the prefix keys are the exact cache: copy them next to the fresh U keys
+    if (p.sq->P > 0)
+      RC_LAUNCH(RC_K_SMALL, 0, 2.0 * p.sq->P * Hk * dh * 2, -1,
+                copy_rows_launch(arena_layer(c, cL, 0), rows, p.sq->arena_row, c->mass_k, rows, p.sq->arena_row,
+                                 p.sq->P, Hk, dh * 2, s));
+  AttnArgs at{};
+  at.q = c->q; at.o = c->o; at.qpos = d_pos; at.tiles = d_ut; at.n_tiles = n_ut;
+  at.k = c->mass_k; at.v = c->mass_v; at.head_stride = rows * dh;
+  at.n_heads = H; at.n_kv_heads = Hk; at.head_dim = dh;
+  at.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
+  at.lse_out = c->mass_lse;
+  RC_LAUNCH(RC_K_ATTN, 0, 0, -1, attn_tc_launch(&c->mQ3, &c->mK_mass, &c->mV_mass, at, rows, s));
+  RC_CUDA(cudaMemsetAsync(c->mass_a, 0, static_cast<size_t>(U) * 8, s));
+  MassArgs ma{};
+  ma.key_tiles = d_kt; ma.n_key_tiles = n_kt; ma.req = d_mreq; ma.lse = c->mass_lse; ma.mass = c->mass_a;
+  ma.n_heads = H; ma.n_kv_heads = Hk; ma.scale_log2 = at.scale_log2;
+  RC_LAUNCH(RC_K_ATTN, 0, 0, -1, attn_mass_launch(&c->mQ3, &c->mK_mass, ma, rows, s));
+  RC_LAUNCH(RC_K_SMALL, 0, U * 16.0, -1, mass_combine_launch(c->dev, c->mass_a, U, static_cast<double>(lam), s));
+  return RC_OK;
+}
+}  // namespace
+
 rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm, float* logits,
                                float* cand_scores, int32_t* sel_pos_out, float* hidden, rc_stream stream) {
   if (!c || n_req <= 0 || !seqs) return fail(RC_E_INVALID, "null argument / empty batch");
@@ -857,6 +921,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   for (auto& p : plan) n_cand += static_cast<int32_t>(p.sq->cand_idtok.size());
   // forced selection (test mode): validate
   const bool forced = prm->forced_sel != nullptr;
+  const bool mass = !forced && prm->lambda < 1.0f;  // NEXT-1: Eq. 3 with the attention-mass term
   if (forced) {
     if (!prm->forced_sel_off) return fail(RC_E_INVALID, "forced_sel needs forced_sel_off");
     for (int r = 0; r < n_req; ++r) {
@@ -885,12 +950,13 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   const int ak = c->attn_tc ? prm->attn_kernel : RC_ATTN_SINGLE;
   int split_u = 1, split_s = 1;
   if (ak == RC_ATTN_SPLIT2) {
-    split_u = split_s = 2;
+    split_u = mass ? 1 : 2;
+    split_s = 2;
   } else if (ak == RC_ATTN_AUTO && c->attn_tc) {
     int64_t ntok = 0;
     for (auto& p : plan) ntok += p.sq->n;
     const int est_kv = static_cast<int>(ntok / n_req / 128) + 1;
-    split_u = attn_tc_choose_splits(n_ut, m.n_kv_heads, est_kv, c->num_sms);
+    split_u = mass ? 1 : attn_tc_choose_splits(n_ut, m.n_kv_heads, est_kv, c->num_sms);  // mass: U tiles feed pass 1
     split_s = attn_tc_choose_splits(n_st, m.n_kv_heads, est_kv, c->num_sms);
   }
   // large grids: two query tiles of one request per CTA share every K/V tile load (k_attn_pair.cu);
@@ -912,6 +978,11 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   const size_t o_ut = lay.add(static_cast<size_t>(n_ut) * 16), o_st = lay.add(static_cast<size_t>(n_st) * 16),
                o_last = lay.add(n_req * 4), o_creq = lay.add(n_cand * 4), o_cid = lay.add(n_cand * 4),
                o_fsel = lay.add(forced ? static_cast<size_t>(S) * 12 : 0);
+  // NEXT-1 key tiles: every 128-key tile of a request that holds U keys; per request {u_off, u_cnt, P, arena_row}
+  int32_t n_kt = 0;
+  if (mass)
+    for (auto& p : plan) n_kt += (p.sq->n + 127) / 128 - p.sq->P / 128;
+  const size_t o_kt = lay.add(static_cast<size_t>(n_kt) * 16), o_mreq = lay.add(mass ? n_req * 16 : 0);
   cudaError_t e;
   const int slot = c->stage.acquire(lay.off, &e);
   if (slot < 0) return fail(RC_E_NOMEM, std::string("staging: ") + cudaGetErrorString(e));
@@ -922,7 +993,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   int4* hreq2 = reinterpret_cast<int4*>(hb + o_req2);
   int4* hut = reinterpret_cast<int4*>(hb + o_ut);
   int4* hst = reinterpret_cast<int4*>(hb + o_st);
-  int iu = 0, is = 0, ic = 0;
+  int iu = 0, is = 0, ic = 0, ikt = 0;
   for (int r = 0; r < n_req; ++r) {
     const ReqPlan& p = plan[r];
     const Seq& sq = *p.sq;
@@ -945,6 +1016,11 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
       for (int sp = 0; sp < split_s; ++sp) hst[is++] = make_int4(p.sel_off + i, std::min(TQ, p.sel_cnt - i), arow, sp);
     if (pair_s && ntiles(p.sel_cnt) % 2) hst[is++] = make_int4(p.sel_off + p.sel_cnt, 0, arow, 0);
     H32(o_last)[r] = p.sel_off + p.sel_cnt - 1;
+    if (mass) {
+      reinterpret_cast<int4*>(hb + o_mreq)[r] = make_int4(p.u_off, p.u_cnt, sq.P, arow);
+      for (int k0 = sq.P / 128 * 128; k0 < sq.n; k0 += 128)
+        reinterpret_cast<int4*>(hb + o_kt)[ikt++] = make_int4(r, k0, std::min(128, sq.n - k0), 0);
+    }
     for (size_t j = 0; j < sq.cand_idtok.size(); ++j) { H32(o_creq)[ic] = r; H32(o_cid)[ic] = sq.cand_idtok[j]; ++ic; }
     if (forced) {
       int32_t* fs = H32(o_fsel);
@@ -990,6 +1066,13 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     RC_LAUNCH(RC_K_GEMM, gemm_flops(U, Nkv, d), gemm_bytes(U, Nkv, d, 2), -1,
               gemm_launch(&c->mA_a, &c->mB_kv[cL], nullptr, U, 2 * m.n_kv_heads * m.head_dim, d, c->bn_kv, EPI_DEV, ev,
                           c->num_sms, s));
+    if (mass) {  // NEXT-1: S = rint((1 - lambda) A + lambda D) over dev
+      st = mass_scores(c, cL, U, D32(o_pos), D32(o_dst), d_ut, n_ut, reinterpret_cast<const int4*>(db + o_kt), n_kt,
+                       reinterpret_cast<const int4*>(db + o_mreq), plan, prm->lambda, s);
+      if (st != RC_OK) return st;
+    }
+    if (prm->score_out)
+      RC_CUDA(cudaMemcpyAsync(prm->score_out, c->dev, static_cast<size_t>(U) * 8, cudaMemcpyDeviceToDevice, s));
     // ---- a4: selection
     SelectArgs sa{};
     sa.dev = c->dev; sa.ucls = reinterpret_cast<const uint8_t*>(db + o_cls);

@@ -101,6 +101,7 @@ struct AttnArgs {
   int32_t n_splits = 1;
   float* part_o = nullptr;   // [n_tiles][Hk][128][128]
   float* part_ml = nullptr;  // [n_tiles][Hk][128][2]
+  float* lse_out = nullptr;  // optional [R][H]: m + log2(l) per query row (k_attn_tc, n_splits = 1; NEXT-1)
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
@@ -115,6 +116,20 @@ cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const
 cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV,
                              const AttnArgs& a, int64_t t_cap, cudaStream_t s);
 bool attn_use_pairs(int n_tiles, int n_kv_heads, int num_sms);
+// NEXT-1 attention mass (k_attn_mass.cu): column sums of the check-layer softmax per key
+struct MassArgs {
+  const int4* key_tiles;  // {request, first key position, keys in tile (<= 128), 0}
+  int32_t n_key_tiles;
+  const int4* req;        // per request {u_off, u_cnt, P (first U position), arena_row}
+  const float* lse;       // [U][H] from pass 1
+  unsigned long long* mass;  // [U] accumulated (zeroed by the caller)
+  int32_t n_heads, n_kv_heads;
+  float scale_log2;
+};
+cudaError_t attn_mass_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const MassArgs& a, int64_t t_cap,
+                             cudaStream_t s);
+cudaError_t mass_combine_launch(unsigned long long* dev, const unsigned long long* mass, int32_t n, double lam,
+                                cudaStream_t s);
 bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
                        uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 

@@ -207,3 +207,47 @@ def test_attention_launch_shapes_match_oracle(wl, attn_kernel):
         assert jac >= 0.8, jac
         assert rel_l2(res["logits"][r], forced["logits"]) < TOL
         assert rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
+
+
+# ----------------------------------------------------------------------------- NEXT-1: attention mass
+@pytest.mark.parametrize("wl,c,lam", [(rcgen.MINI_L, 0, 0.5), (rcgen.MINI_L, 1, 0.5), (rcgen.MINI_Q, 1, 0.0),
+                                      (rcgen.MINI_Q, 0, 0.25)])
+def test_attention_mass_scores_and_selection(wl, c, lam):
+    """Eq. 3 with lambda < 1 (R2 / R2-FX): the GPU's scores S of every U row against
+    the oracle's, selection bit-exact given the GPU's own scores, and the selective result against
+    O-SEL forced to the GPU's selection, on a 2-request ragged batch."""
+    G = _gpu()
+    case = make_case(wl, n_req=2)
+    pools = oracle_pools(case)
+    olays = layouts(case)
+    n_tok = sum(l.n for l in olays)
+    ctx, _ = G.make_ctx(case, pools, n_tok)
+    lays = G.gpu_layouts(ctx, case)
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=c)
+    ucnt = [int((l["cls"] != PREFIX).sum()) for l in lays]
+    score = torch.zeros(sum(ucnt), dtype=torch.int64, device="cuda")
+    n_cand = sum(len(l["cand_idtok"]) for l in lays)
+    out = ctx.selective_prefill(seqs, 1500, 1500, check_layer=c, lam=lam, hidden=True, n_cand=n_cand, score_out=score)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
+    S_all = score.cpu().numpy().view(np.uint64)
+    ctx.release(seqs)
+    ctx.close()
+    u0 = 0
+    for r, lay in enumerate(olays):
+        P = lay.n - ucnt[r]
+        S_gpu = np.zeros(lay.n, np.uint64)
+        S_gpu[P:] = S_all[u0:u0 + ucnt[r]]
+        u0 += ucnt[r]
+        sel = res["sel_pos"][res["sel_off"][r]:res["sel_off"][r + 1]]
+        assert np.array_equal(sel, select_sel(lay.cls, S_gpu, 1500, 1500, 0))
+        m = OracleModel(case["shape"], case["W"])
+        K, V, _ = assemble(case["shape"], lay, pools["items"], pools["hist"], pools["prefix"], gather_from=c)
+        own = selective_prefill(m, lay, K, V, 1500, 1500, check_layer=c, lam=lam)
+        forced = selective_prefill(m, lay, K, V, 1500, 1500, check_layer=c, lam=lam, forced_sel=sel)
+        reuse = np.isin(lay.cls, [HIST, ITEM])
+        assert rel_l2(S_gpu[reuse].astype(np.float64), own["S"][reuse].astype(np.float64)) < 2e-2
+        jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
+        assert jac >= 0.8, jac
+        assert rel_l2(res["logits"][r], forced["logits"]) < TOL
+        assert rel_l2(res["hidden"][res["sel_off"][r]:res["sel_off"][r + 1]], forced["x_sel"]) < TOL
