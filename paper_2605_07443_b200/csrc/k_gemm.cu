@@ -119,44 +119,67 @@ __device__ __forceinline__ void add_bias(float* v, const uint16_t* b, int n) {
 #pragma unroll
     for (int j = 0; j < n; ++j) v[j] += bf2f(b[j]);
 }
-// Fused QKV / deviation epilogue over the heads of one tile (templated on the RoPE chunk width).
-template <int BN, int CW, bool DEV>
+// Per-row RoPE state of the fused QKV / deviation epilogue: position, stitched-arena row and the
+// fp32 cos/sin of the row's position, loaded BEFORE the epilogue waits for the accumulator so
+// the table reads overlap the tile's main loop instead of stalling every 16-column chunk.
+template <int DH>
+struct RopeRow {
+  int pos = 0, drow = 0;
+  float cs[DH / 2], sn[DH / 2];
+};
+template <int DH>
+__device__ __forceinline__ void rope_row_load(RopeRow<DH>& rr, int row, bool row_ok, const EpiArgs& ep) {
+  if (!row_ok) return;
+  rr.pos = __ldg(ep.pos + row);
+  rr.drow = __ldg(ep.dst_row + row);
+  const float4* c4 = reinterpret_cast<const float4*>(ep.rope_cos + static_cast<int64_t>(rr.pos + ep.rope_zero) * (DH / 2));
+  const float4* s4 = reinterpret_cast<const float4*>(ep.rope_sin + static_cast<int64_t>(rr.pos + ep.rope_zero) * (DH / 2));
+#pragma unroll
+  for (int i = 0; i < DH / 8; ++i) {
+    const float4 c = __ldg(c4 + i), sv = __ldg(s4 + i);
+    rr.cs[4 * i] = c.x; rr.cs[4 * i + 1] = c.y; rr.cs[4 * i + 2] = c.z; rr.cs[4 * i + 3] = c.w;
+    rr.sn[4 * i] = sv.x; rr.sn[4 * i + 1] = sv.y; rr.sn[4 * i + 2] = sv.z; rr.sn[4 * i + 3] = sv.w;
+  }
+}
+
+// Fused QKV / deviation epilogue over the heads of one tile (DH compile-time: every chunk index
+// is a constant, so the RoPE row stays in registers).
+template <int BN, int DH, bool DEV>
 __device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool row_ok, int row, const EpiArgs& ep,
-                                          unsigned long long& dev_acc) {
-  const int dh = ep.head_dim;
+                                          const RopeRow<DH>& rr, unsigned long long& dev_acc) {
+  constexpr int CW = DH >= 32 ? 16 : 8;
   const int H = DEV ? 0 : ep.n_heads;
   const int Hk = ep.n_kv_heads;
-  int pos = 0, drow = 0;
-  if (row_ok) { pos = ep.pos[row]; drow = ep.dst_row[row]; }
-  const float* cs_row = ep.rope_cos + static_cast<int64_t>(pos + ep.rope_zero) * (dh / 2);
-  const float* sn_row = ep.rope_sin + static_cast<int64_t>(pos + ep.rope_zero) * (dh / 2);
-  const int heads_in_tile = BN / dh;
+  const int drow = rr.drow;
+  constexpr int heads_in_tile = BN / DH;
+#pragma unroll 1
   for (int hi = 0; hi < heads_in_tile; ++hi) {
-    const int hh = n0 / dh + hi;  // head index in the packed output
-    if (hh * dh >= N) break;
-    const int col0 = hi * dh;
+    const int hh = n0 / DH + hi;  // head index in the packed output
+    if (hh * DH >= N) break;
+    const int col0 = hi * DH;
     const bool is_q = hh < H;
     const bool is_k = !is_q && hh < H + Hk;
-    const uint16_t* bias = ep.bias ? ep.bias + hh * dh : nullptr;
+    const uint16_t* bias = ep.bias ? ep.bias + hh * DH : nullptr;
     if (is_q || is_k) {
       uint16_t* dst;
       const uint16_t* st = nullptr;
-      if (is_q) dst = ep.q_out + static_cast<int64_t>(row) * ep.q_ld + hh * dh;
+      if (is_q) dst = ep.q_out + static_cast<int64_t>(row) * ep.q_ld + hh * DH;
       else {
-        const int64_t off = static_cast<int64_t>(hh - H) * ep.head_stride + static_cast<int64_t>(drow) * dh;
+        const int64_t off = static_cast<int64_t>(hh - H) * ep.head_stride + static_cast<int64_t>(drow) * DH;
         dst = ep.arena_k + off;
         st = ep.arena_k + off;
       }
-      for (int c = 0; c < dh / 2; c += CW) {
+#pragma unroll
+      for (int c = 0; c < DH / 2; c += CW) {
         float lo[CW], hv[CW];
         tmem_ldCW<CW>(taddr + col0 + c, lo);
-        tmem_ldCW<CW>(taddr + col0 + dh / 2 + c, hv);
+        tmem_ldCW<CW>(taddr + col0 + DH / 2 + c, hv);
         if (!row_ok) continue;
-        if (bias) { add_bias(lo, bias + c, CW); add_bias(hv, bias + dh / 2 + c, CW); }
+        if (bias) { add_bias(lo, bias + c, CW); add_bias(hv, bias + DH / 2 + c, CW); }
         float y0[CW], y1[CW];
 #pragma unroll
         for (int j = 0; j < CW; ++j) {
-          const float cc = cs_row[c + j], ss = sn_row[c + j];
+          const float cc = rr.cs[c + j], ss = rr.sn[c + j];
           y0[j] = __fsub_rn(__fmul_rn(lo[j], cc), __fmul_rn(hv[j], ss));
           y1[j] = __fadd_rn(__fmul_rn(hv[j], cc), __fmul_rn(lo[j], ss));
         }
@@ -164,17 +187,18 @@ __device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool ro
 #pragma unroll
           for (int j = 0; j < CW; ++j) {
             dev_acc += dev_term(y0[j], st[c + j]);
-            dev_acc += dev_term(y1[j], st[dh / 2 + c + j]);
+            dev_acc += dev_term(y1[j], st[DH / 2 + c + j]);
           }
         } else {
           st_bf16xCW<CW>(dst + c, y0);
-          st_bf16xCW<CW>(dst + dh / 2 + c, y1);
+          st_bf16xCW<CW>(dst + DH / 2 + c, y1);
         }
       }
     } else {  // V head: no rotation
-      const int64_t off = static_cast<int64_t>(hh - H - Hk) * ep.head_stride + static_cast<int64_t>(drow) * dh;
+      const int64_t off = static_cast<int64_t>(hh - H - Hk) * ep.head_stride + static_cast<int64_t>(drow) * DH;
       uint16_t* dst = ep.arena_v + off;
-      for (int c = 0; c < dh; c += CW) {
+#pragma unroll
+      for (int c = 0; c < DH; c += CW) {
         float v[CW];
         tmem_ldCW<CW>(taddr + col0 + c, v);
         if (!row_ok) continue;
@@ -244,14 +268,33 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
       for (int j = 0; j < 16; ++j) g[j] = g[j] / (1.0f + __expf(-g[j])) * u[j];
       st_bf16x16(static_cast<uint16_t*>(ep.out) + static_cast<int64_t>(row) * ep.ldo + n0 / 2 + c, g);
     }
-  } else {
-    constexpr bool DEV = (EPI == EPI_DEV);
-    unsigned long long acc = 0;
-    if (ep.head_dim >= 32) epi_heads<BN, 16, DEV>(taddr, n0, N, row_ok, row, ep, acc);
-    else epi_heads<BN, 8, DEV>(taddr, n0, N, row_ok, row, ep, acc);
+  }
+}
+
+// QKV / deviation tiles: the RoPE row of the next tile is loaded before waiting for its accumulator
+template <int BN, int DH, int EPI>
+__device__ __forceinline__ void epilogue_heads_loop(uint32_t tmem_base, int q, int M, int N, int units, int splits,
+                                                    int num_m, int num_n, int group_m, uint64_t* tfull,
+                                                    uint64_t* tempty, const EpiArgs& ep) {
+  constexpr bool DEV = (EPI == EPI_DEV);
+  int it = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+    int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
+    const int row = mb * BM + q * 32 + (threadIdx.x & 31);
+    const bool row_ok = row < M;
+    RopeRow<DH> rr;
+    rope_row_load<DH>(rr, row, row_ok, ep);
+    const int acc = it & 1;
+    mbar_wait(&tfull[acc], (it >> 1) & 1);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+    unsigned long long dacc = 0;
+    epi_heads<BN, DH, DEV>(taddr, nb * BN, N, row_ok, row, ep, rr, dacc);
     if constexpr (DEV) {
-      if (row_ok && ep.row_reuse[row]) atomicAdd(ep.dev_out + row, acc);
+      if (row_ok && ep.row_reuse[row]) atomicAdd(ep.dev_out + row, dacc);
     }
+    tc_fence_before();
+    mbar_arrive(&tempty[acc]);
   }
 }
 
@@ -332,6 +375,14 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&tfull[acc]);
       }
     }
+  } else if (warp >= 4 && (EPI == EPI_QKV || EPI == EPI_DEV)) {  // ---------------- QKV / deviation epilogue
+    const int q = warp & 3;
+    if (ep.head_dim == 128)
+      epilogue_heads_loop<BN, 128, EPI>(tmem_base, q, M, N, units, splits, num_m, num_n, group_m, tfull, tempty, ep);
+    else if (ep.head_dim == 64)
+      epilogue_heads_loop<BN, 64, EPI>(tmem_base, q, M, N, units, splits, num_m, num_n, group_m, tfull, tempty, ep);
+    else
+      epilogue_heads_loop<BN, 16, EPI>(tmem_base, q, M, N, units, splits, num_m, num_n, group_m, tfull, tempty, ep);
   } else if (warp >= 4) {  // ---------------- epilogue warps
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     int it = 0, chunk_ctr = 0;
