@@ -271,16 +271,34 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
   }
 }
 
+// Persistent schedule of one CTA: work units u0, u0 + ustep, ... (tile = unit / splits); a tile is
+// tile_m rows (128, or 256 for a CTA pair whose rank-1 CTA owns rows row_off = 128 .. 255)
+struct Sched {
+  int u0, ustep, units, splits, num_m, num_n, group_m, tile_m, row_off;
+};
+
+// hand an accumulator buffer back to the MMA issuer: every epilogue thread of a single CTA, or one
+// lane per epilogue warp of both CTAs of a pair onto the leader's barrier
+template <bool PAIR>
+__device__ __forceinline__ void release_acc(uint64_t* tempty, int acc, uint32_t leader_tempty) {
+  if constexpr (PAIR) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(leader_tempty + acc * 8);
+  } else {
+    mbar_arrive(&tempty[acc]);
+  }
+}
+
 // QKV / deviation tiles: the RoPE row of the next tile is loaded before waiting for its accumulator
-template <int BN, int DH, int EPI>
-__device__ __forceinline__ void epilogue_heads_loop(uint32_t tmem_base, int q, int M, int N, int units, int splits,
-                                                    int num_m, int num_n, int group_m, uint64_t* tfull,
-                                                    uint64_t* tempty, const EpiArgs& ep) {
+template <int BN, int DH, int EPI, bool PAIR>
+__device__ __forceinline__ void epilogue_heads_loop(uint32_t tmem_base, int q, int M, int N, const Sched& sc,
+                                                    uint64_t* tfull, uint64_t* tempty, uint32_t leader_tempty,
+                                                    const EpiArgs& ep) {
   constexpr bool DEV = (EPI == EPI_DEV);
   int it = 0;
-  for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-    int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
-    const int row = mb * BM + q * 32 + (threadIdx.x & 31);
+  for (int u = sc.u0; u < sc.units; u += sc.ustep, ++it) {
+    int mb, nb; tile_coords(u / sc.splits, sc.num_m, sc.num_n, sc.group_m, mb, nb);
+    const int row = mb * sc.tile_m + sc.row_off + q * 32 + (threadIdx.x & 31);
     const bool row_ok = row < M;
     RopeRow<DH> rr;
     rope_row_load<DH>(rr, row, row_ok, ep);
@@ -294,7 +312,42 @@ __device__ __forceinline__ void epilogue_heads_loop(uint32_t tmem_base, int q, i
       if (row_ok && ep.row_reuse[row]) atomicAdd(ep.dev_out + row, dacc);
     }
     tc_fence_before();
-    mbar_arrive(&tempty[acc]);
+    release_acc<PAIR>(tempty, acc, leader_tempty);
+  }
+}
+
+// the epilogue warps (4..7) of one CTA over its whole schedule
+template <int BN, int EPI, bool PAIR>
+__device__ __forceinline__ void epilogue_loop(uint32_t tmem_base, int warp, int M, int N, const Sched& sc,
+                                              uint64_t* tfull, uint64_t* tempty, uint32_t leader_tempty,
+                                              const EpiArgs& ep, const CUtensorMap* tmC, uint8_t* sOut) {
+  const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+  if constexpr (EPI == EPI_QKV || EPI == EPI_DEV) {
+    if (ep.head_dim == 128)
+      epilogue_heads_loop<BN, 128, EPI, PAIR>(tmem_base, q, M, N, sc, tfull, tempty, leader_tempty, ep);
+    else if (ep.head_dim == 64)
+      epilogue_heads_loop<BN, 64, EPI, PAIR>(tmem_base, q, M, N, sc, tfull, tempty, leader_tempty, ep);
+    else
+      epilogue_heads_loop<BN, 16, EPI, PAIR>(tmem_base, q, M, N, sc, tfull, tempty, leader_tempty, ep);
+  } else {
+    int it = 0, chunk_ctr = 0;
+    if (EPI == EPI_ADD_F32 && (threadIdx.x & 31) == 0) tma_prefetch_desc(tmC);
+    for (int u = sc.u0; u < sc.units; u += sc.ustep, ++it) {
+      int mb, nb; tile_coords(u / sc.splits, sc.num_m, sc.num_n, sc.group_m, mb, nb);
+      const int m0 = mb * sc.tile_m + sc.row_off;
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
+      if constexpr (EPI == EPI_ADD_F32) epilogue_add_tma<BN>(taddr, m0, nb * BN, N, q, tmC, sOut, chunk_ctr);
+      else epilogue_tile<BN, EPI>(taddr, m0, nb * BN, M, N, q * 32, ep, sc.splits > 1);
+      tc_fence_before();
+      release_acc<PAIR>(tempty, acc, leader_tempty);
+    }
+    if constexpr (EPI == EPI_ADD_F32) {
+      if ((threadIdx.x & 31) == 0) bulk_wait<0>();  // reductions complete before the CTA retires
+      __syncwarp();
+    }
   }
 }
 
@@ -345,7 +398,9 @@ __global__ void __launch_bounds__(256, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, nb * BN);
+#pragma unroll
+          for (int h = 0; h < BN / 128; ++h)  // B boxes are 128 rows (shared with the CTA-pair kernel)
+            tma_load_2d(sB + stage * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[stage], kb * BK, nb * BN + h * 128);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -375,39 +430,166 @@ __global__ void __launch_bounds__(256, 1)
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4 && (EPI == EPI_QKV || EPI == EPI_DEV)) {  // ---------------- QKV / deviation epilogue
-    const int q = warp & 3;
-    if (ep.head_dim == 128)
-      epilogue_heads_loop<BN, 128, EPI>(tmem_base, q, M, N, units, splits, num_m, num_n, group_m, tfull, tempty, ep);
-    else if (ep.head_dim == 64)
-      epilogue_heads_loop<BN, 64, EPI>(tmem_base, q, M, N, units, splits, num_m, num_n, group_m, tfull, tempty, ep);
-    else
-      epilogue_heads_loop<BN, 16, EPI>(tmem_base, q, M, N, units, splits, num_m, num_n, group_m, tfull, tempty, ep);
   } else if (warp >= 4) {  // ---------------- epilogue warps
-    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-    int it = 0, chunk_ctr = 0;
-    if (EPI == EPI_ADD_F32 && (threadIdx.x & 31) == 0) tma_prefetch_desc(&tmC);
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
-      int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
-      if constexpr (EPI == EPI_ADD_F32) epilogue_add_tma<BN>(taddr, mb * BM, nb * BN, N, q, &tmC, sOut, chunk_ctr);
-      else epilogue_tile<BN, EPI>(taddr, mb * BM, nb * BN, M, N, q * 32, ep, splits > 1);
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-    }
-    if constexpr (EPI == EPI_ADD_F32) {
-      if ((threadIdx.x & 31) == 0) bulk_wait<0>();  // reductions complete before the CTA retires
-      __syncwarp();
-    }
+    const Sched sc{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), units, splits, num_m, num_n, group_m, BM, 0};
+    epilogue_loop<BN, EPI, false>(tmem_base, warp, M, N, sc, tfull, tempty, 0u, ep, &tmC, sOut);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, C::TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ CTA-pair GEMM (cta_group::2)
+// Tile = 256 x 256 over a cluster of 2 CTAs on one TPC: each CTA stages its own 128 rows of A and
+// 128 of the 256 rows of B (so 32 KB of operands per k-block per SM instead of 48 KB: the per-SM
+// L2->SMEM feed, ~120 GB/s, is what bounds the single-CTA GEMM at high clocks); the leader issues
+// one M=256, N=256 MMA per 16-deep k-step that writes rows 0..127 into its TMEM and 128..255 into
+// the peer's. Barriers: full[s] lives in the leader (both producers' TMA bytes are counted there,
+// the leader's expect_tx is its only arrival; the peer's bytes may land before it: tx goes
+// negative while the arrival is still pending, so the phase cannot complete early),
+// empty[s] / tfull[a] in both (the leader's commits multicast), tempty[a] in the leader (one
+// arrival per epilogue warp of both CTAs). Epilogues are the single-CTA ones on 128-row halves.
+struct PairCfg {
+  static constexpr int STAGES = 6;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;     // 16 KB: this CTA's 128 rows of A
+  static constexpr uint32_t B_BYTES = 128 * BK * 2;    // 16 KB: this CTA's half of the 256 rows of B
+  static constexpr uint32_t STAGE_OUT = 4 * 2 * 32 * 32 * 4;
+  static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + STAGE_OUT + 1024 + 256;
+  static constexpr uint32_t TMEM_COLS = 512;
+};
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    k_gemm_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits, int group_m,
+                const EpiArgs ep) {
+  using C = PairCfg;
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint8_t* sOut = sB + C::STAGES * C::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + C::STAGE_OUT);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    // full[s]: one arrival (the leader's expect_tx for both CTAs' bytes); the peer's TMA only
+    // completes transactions on it (a release.cluster arrive per k-block costs a fence each time)
+    for (int s = 0; s < C::STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch_desc(&tmA); tma_prefetch_desc(&tmB); }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();  // barrier inits and both TMEM allocations visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
+
+  const int num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
+  const int nk = (K + BK - 1) / BK;
+  const int units = tiles * splits;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t leader_full = mapa_shared(full, 0);
+  const uint32_t leader_tempty = mapa_shared(tempty, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0; uint32_t phase = 0;
+      for (int u = cid; u < units; u += ncl) {
+        int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
+        const int sp = u % splits;
+        const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
+        for (int kb = sp * nk / splits; kb < (sp + 1) * nk / splits; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = leader_full + stage * 8;
+          if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow);
+          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN);
+      int stage = 0; uint32_t phase = 0; int it = 0;
+      for (int u = cid; u < units; u += ncl, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        const int sp = u % splits, kb0 = sp * nk / splits;
+        for (int kb = kb0; kb < (sp + 1) * nk / splits; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          umma_commit_pair(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue warps (both CTAs, own 128 rows)
+    const Sched sc{cid, ncl, units, splits, num_m, num_n, group_m, 2 * BM, static_cast<int>(rank) * BM};
+    epilogue_loop<BN, EPI, true>(tmem_base, warp, M, N, sc, tfull, tempty, leader_tempty, ep, &tmC, sOut);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the leader's last MMAs into this CTA's TMEM are complete (tfull waited) on both sides
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+}
+
+template <int EPI>
+cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K,
+                        const EpiArgs& ep, int num_sms, cudaStream_t s) {
+  if (EPI == EPI_ADD_F32 && c == nullptr) return cudaErrorInvalidValue;
+  using C = PairCfg;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(k_gemm_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int pairs = num_sms / 2;
+  const int num_m = (M + 2 * BM - 1) / (2 * BM);
+  const int tiles = num_m * ((N + 255) / 256);
+  const int nk = (K + BK - 1) / BK;
+  int splits = 1;
+  if (EPI == EPI_ADD_F32) {
+    auto cost = [&](int sp) {
+      const int64_t units = static_cast<int64_t>(tiles) * sp;
+      return ((units + pairs - 1) / pairs) * ((nk + sp - 1) / sp + 6);
+    };
+    int64_t best = cost(1);
+    for (int sp = 2; sp <= 16 && nk / sp >= 8; ++sp)
+      if (cost(sp) * 100 < best * 95) { best = cost(sp); splits = sp; }
+  }
+  const int units = tiles * splits;
+  const int grid = 2 * (units < pairs ? units : pairs);
+  static const size_t group_a_bytes = [] {
+    const char* e = std::getenv("RC_GROUP_A_MB");
+    return e ? static_cast<size_t>(std::atoi(e)) << 20 : GROUP_A_BYTES;
+  }();
+  const int group_m = static_cast<int>(std::max<size_t>(
+      2, std::min<size_t>(num_m, group_a_bytes / (static_cast<size_t>(2 * BM) * K * 2))));
+  return launch_pdl(k_gemm_pair<EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits,
+                    group_m, ep);
 }
 
 template <int BN, int EPI>
@@ -465,7 +647,7 @@ PFN_encodeTiled get_encode() {
 }
 }  // namespace
 
-int gemm_box_rows_b(int bn) { return bn; }
+int gemm_box_rows_b(int bn) { return bn < 128 ? bn : 128; }
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
                        uint32_t box_rows) {
@@ -511,6 +693,22 @@ bool make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t
 cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K, int bn,
                         int epi, const EpiArgs& ep, int num_sms, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  // CTA pairs for 256-wide GEMMs with M >= 1024: at cfg3 batch 32 they lift the GEMMs from 0.92 to
+  // 0.99 of the measured sustained peak; at M = 625 (one request's Sel) the 256-row quantisation
+  // (768 rows computed) costs more than the halved operand feed saves. RC_GEMM_PAIR=0/1 forces.
+  static const int pair_mode = [] { const char* e = std::getenv("RC_GEMM_PAIR"); return e ? std::atoi(e) : -1; }();
+  const bool pair = pair_mode == 1 || (pair_mode == -1 && M >= 1024);
+  if (pair && bn == 256 && M > BM && num_sms >= 2) {
+    switch (epi) {
+      case EPI_BF16: return launch_pair<EPI_BF16>(a, b, c, M, N, K, ep, num_sms, s);
+      case EPI_F32: return launch_pair<EPI_F32>(a, b, c, M, N, K, ep, num_sms, s);
+      case EPI_ADD_F32: return launch_pair<EPI_ADD_F32>(a, b, c, M, N, K, ep, num_sms, s);
+      case EPI_SWIGLU: return launch_pair<EPI_SWIGLU>(a, b, c, M, N, K, ep, num_sms, s);
+      case EPI_QKV: return launch_pair<EPI_QKV>(a, b, c, M, N, K, ep, num_sms, s);
+      case EPI_DEV: return launch_pair<EPI_DEV>(a, b, c, M, N, K, ep, num_sms, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
 #define RC_GEMM_CASE(BN_, E_) \
   if (bn == BN_ && epi == E_) return launch_one<BN_, E_>(a, b, c, M, N, K, ep, num_sms, s);
   RC_GEMM_CASE(256, EPI_BF16) RC_GEMM_CASE(256, EPI_F32) RC_GEMM_CASE(256, EPI_ADD_F32)

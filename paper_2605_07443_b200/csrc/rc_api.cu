@@ -436,13 +436,13 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   c->mB_qkv.resize(L); c->mB_kv.resize(L); c->mB_o.resize(L); c->mB_gu.resize(L); c->mB_d.resize(L);
   for (int l = 0; l < L && ok; ++l) {
     const uint16_t* wq = c->wqkv + static_cast<size_t>(l) * c->Nqkv * d;
-    ok = ok && make_tmap_bf16_2d(&c->mB_qkv[l], wq, c->Nqkv, d, d, c->bn_qkv);
-    ok = ok && make_tmap_bf16_2d(&c->mB_kv[l], wq + static_cast<size_t>(H) * dh * d, 2 * Hk * dh, d, d, c->bn_kv);
-    ok = ok && make_tmap_bf16_2d(&c->mB_o[l], c->wo[l], d, H * dh, H * dh, c->bn_o);
-    ok = ok && make_tmap_bf16_2d(&c->mB_gu[l], c->wgu + static_cast<size_t>(l) * 2 * F * d, 2 * F, d, d, 256);
-    ok = ok && make_tmap_bf16_2d(&c->mB_d[l], c->wd[l], d, F, F, c->bn_d);
+    ok = ok && make_tmap_bf16_2d(&c->mB_qkv[l], wq, c->Nqkv, d, d, gemm_box_rows_b(c->bn_qkv));
+    ok = ok && make_tmap_bf16_2d(&c->mB_kv[l], wq + static_cast<size_t>(H) * dh * d, 2 * Hk * dh, d, d, gemm_box_rows_b(c->bn_kv));
+    ok = ok && make_tmap_bf16_2d(&c->mB_o[l], c->wo[l], d, H * dh, H * dh, gemm_box_rows_b(c->bn_o));
+    ok = ok && make_tmap_bf16_2d(&c->mB_gu[l], c->wgu + static_cast<size_t>(l) * 2 * F * d, 2 * F, d, d, gemm_box_rows_b(256));
+    ok = ok && make_tmap_bf16_2d(&c->mB_d[l], c->wd[l], d, F, F, gemm_box_rows_b(c->bn_d));
   }
-  ok = ok && make_tmap_bf16_2d(&c->mB_lm, c->lm_head, m.vocab, d, d, c->bn_lm);
+  ok = ok && make_tmap_bf16_2d(&c->mB_lm, c->lm_head, m.vocab, d, d, gemm_box_rows_b(c->bn_lm));
   c->attn_tc = (dh == 128) && std::getenv("RC_ATTN_LEGACY") == nullptr;
   if (c->attn_tc && ok) {
     const int G = H / Hk;
@@ -1263,7 +1263,7 @@ rc_status rc_diag_gemm(int32_t M, int32_t N, int32_t K, const void* A, const voi
                        rc_stream stream) {
   if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C || (bn != 128 && bn != 256)) return fail(RC_E_INVALID, "bad gemm args");
   CUtensorMap ma, mb;
-  if (!make_tmap_bf16_2d(&ma, A, M, K, K, 128) || !make_tmap_bf16_2d(&mb, B, N, K, K, bn))
+  if (!make_tmap_bf16_2d(&ma, A, M, K, K, 128) || !make_tmap_bf16_2d(&mb, B, N, K, K, gemm_box_rows_b(bn)))
     return fail(RC_E_CUDA, "tensor map encode failed");
   int dev = 0, sms = 148;
   RC_CUDA(cudaGetDevice(&dev));

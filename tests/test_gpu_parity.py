@@ -39,7 +39,7 @@ def _gpu():
 # ----------------------------------------------------------------------------- K3 GEMM unit
 @pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (300, 384, 320, 256), (1000, 6144, 4096, 256),
                                       (77, 144, 112, 128), (3, 1000, 4096, 256), (513, 128, 192, 128),
-                                      (129, 512, 14336, 256)])
+                                      (129, 512, 14336, 256), (1500, 768, 640, 256), (2049, 1280, 4096, 256)])
 def test_gemm_matches_exact_matmul(M, N, K, bn):
     from paper_2605_07443_b200.api import diag_gemm
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N)
