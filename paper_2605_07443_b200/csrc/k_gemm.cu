@@ -697,7 +697,8 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   // 0.99 of the measured sustained peak; at M = 625 (one request's Sel) the 256-row quantisation
   // (768 rows computed) costs more than the halved operand feed saves. RC_GEMM_PAIR=0/1 forces.
   static const int pair_mode = [] { const char* e = std::getenv("RC_GEMM_PAIR"); return e ? std::atoi(e) : -1; }();
-  const bool pair = pair_mode == 1 || (pair_mode == -1 && M >= 1024);
+  // (the residual GEMMs split K over pairs; measured at M = 625 they gain 7% even with the padding)
+  const bool pair = pair_mode == 1 || (pair_mode == -1 && (M >= 1024 || (epi == EPI_ADD_F32 && M > 2 * BM)));
   if (pair && bn == 256 && M > BM && num_sms >= 2) {
     switch (epi) {
       case EPI_BF16: return launch_pair<EPI_BF16>(a, b, c, M, N, K, ep, num_sms, s);
