@@ -136,7 +136,10 @@ typedef struct rc_prefill_params {
                                  the selection score of every U row (Eq. 3 fixed point, DESIGN.md
                                  R4 / R2-FX; only HIST/ITEM rows are meaningful); NULL = none */
 } rc_prefill_params;
-enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3 };
+enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3, RC_ATTN_ADAPTIVE = 4 };
+/* RC_ATTN_SPLIT2: every query tile's KV range in two CTAs + merge; RC_ATTN_ADAPTIVE: the same launch,
+   but tiles shorter than half the longest prompt's KV run unsplit (decided on the device from the
+   selected positions; measured slower than unsplit at cfg3 batch 1, so AUTO does not choose it) */
 
 /* ---------------------------------------------------------------- lifecycle */
 rc_status rc_create(const rc_model_desc* m, const rc_weights* w, const rc_pool_desc* p, int32_t device,

@@ -82,8 +82,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int H = a.n_heads;
   const int max_pos = n_rows > 0 ? a.qpos[row_start + n_rows - 1] : -1;
   const int nkv_all = n_rows > 0 ? max_pos / BKV + 1 : 0;  // padded (empty) tiles do nothing
-  const int j0 = tile.w * nkv_all / a.n_splits;         // this split's KV tiles [j0, j0 + nkv)
-  const int nkv = (tile.w + 1) * nkv_all / a.n_splits - j0;
+  // adaptive 2-way split (split_min > 0): a tile shorter than split_min KV tiles runs unsplit in its
+  // first CTA, which writes O directly; its second CTA has nothing to do
+  const bool short_tile = a.split_min > 0 && nkv_all < a.split_min;
+  const int nsp = short_tile ? 1 : a.n_splits;
+  const bool idle = short_tile && tile.w != 0;
+  const int j0 = idle ? 0 : tile.w * nkv_all / nsp;     // this split's KV tiles [j0, j0 + nkv)
+  const int nkv = idle ? 0 : (tile.w + 1) * nkv_all / nsp - j0;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- Q + K producer
@@ -225,13 +230,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&pv_done[1 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
     }
     tc_fence_after();
-    const bool split = a.n_splits > 1;
+    const bool split = nsp > 1;
+    if (a.split_min > 0 && tile.w == 0 && r == 0 && h == 0)
+      a.split_flag[(blockIdx.x / a.n_splits) * a.n_kv_heads + kvh] = split ? 1 : 0;
     // this thread writes output columns [h*64, h*64 + 64) of its row: bf16 into o, or (KV split) the
     // fp32 partial normalised by its own l plus (m, l) for the merge kernel
     uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + h * 64;
     const int64_t prow = (static_cast<int64_t>(blockIdx.x) * a.n_kv_heads + kvh) * ROWS + r;
     float* pdst = split ? a.part_o + prow * DH + h * 64 : nullptr;
-    if (split && h == 0) {
+    if (split && h == 0 && !idle) {
       a.part_ml[prow * 2] = m;
       a.part_ml[prow * 2 + 1] = nkv > 0 ? l_tot : 0.f;
     }
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_ld32(tmem + lane_base + O_COL + 128 + h * 64 + c, o1);
         tmem_wait_ld();
       }
-      if (valid) {
+      if (valid && !idle) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           float y[8];
@@ -276,6 +283,7 @@ __global__ void __launch_bounds__(256) k_attn_merge(const AttnArgs a) {
   griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
   griddep_launch();
   const int t_log = blockIdx.x, kvh = blockIdx.y, S = a.n_splits;
+  if (a.split_min > 0 && a.split_flag[t_log * a.n_kv_heads + kvh] == 0) return;  // ran unsplit: O written
   const int4 tile = a.tiles[t_log * S];
   const int G = a.n_heads / a.n_kv_heads, TQ = ROWS / G;
   // blockIdx.z picks a 16-row slab: 16 rows x 16 chunks = one unit per thread, so every split's
@@ -334,7 +342,8 @@ cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const
   return launch_pdl(k_attn_merge, dim3(a.n_tiles / a.n_splits, a.n_kv_heads, ROWS / 16), dim3(256), 0, s, a);
 }
 
-int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms) {
+int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms, int* split_min) {
+  *split_min = 0;
   // Split only grids that leave more than half the machine idle. Measured at cfg3 batch 1 (176
   // CTAs, ~1.2 waves): a uniform 2-way split costs +0.35 ms over 32 launches, because the split
   // shares are uniform while the causal KV lengths are not and the extra partial write + merge
@@ -347,6 +356,8 @@ int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num
   const int64_t units = static_cast<int64_t>(n_tiles) * n_kv_heads;
   int best = 1;
   while (best < 8 && units * (best * 2) <= num_sms && est_kv_tiles / (best * 2) >= 4) best *= 2;
+  // (an adaptive split of only the long tiles -- RC_ATTN_ADAPTIVE -- was measured at cfg3 batch 1:
+  // 2.16 vs 2.03 ms per step, because the doubled grid runs in two full waves; not chosen here)
   return best;
 }
 

@@ -209,6 +209,7 @@ struct rc_ctx {
   int64_t logits_rows = 0;
   float* part_o = nullptr;   // KV-split attention partials
   float* part_ml = nullptr;
+  int32_t* part_flag = nullptr;  // adaptive split: which logical tiles were split
   size_t part_rows = 0;
   int32_t* sel_pos = nullptr;
   int32_t* sel_dst = nullptr;
@@ -248,7 +249,7 @@ struct rc_ctx {
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
-                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, mass_k, mass_v,
+                    a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
                     mass_lse, mass_a};
     for (void* p : bufs)
       if (p) cudaFree(p);
@@ -786,7 +787,8 @@ rc_status rc_sel_count(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_pr
 namespace {
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
 rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
-                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, bool paired,
+                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min,
+                    bool paired,
                     double attn_flops, int attn_pending, cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
@@ -810,19 +812,23 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
   static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
   at.debug_mode = attn_debug;
   at.n_splits = n_splits;
+  at.split_min = split_min;
   if (n_splits > 1) {  // partial-output workspace, grown on first use
     const size_t need = static_cast<size_t>(n_tiles) * Hk * 128;
     if (c->part_rows < need) {
       if (c->part_o) cudaFree(c->part_o);
       if (c->part_ml) cudaFree(c->part_ml);
+      if (c->part_flag) cudaFree(c->part_flag);
       cudaError_t e;
       c->part_o = dev_alloc<float>(need * 128, &e);
       if (e == cudaSuccess) c->part_ml = dev_alloc<float>(need * 2, &e);
+      if (e == cudaSuccess) c->part_flag = dev_alloc<int32_t>(static_cast<size_t>(n_tiles) * Hk, &e);
       if (e != cudaSuccess) { c->part_rows = 0; return fail(RC_E_NOMEM, "attention split workspace"); }
       c->part_rows = need;
     }
     at.part_o = c->part_o;
     at.part_ml = c->part_ml;
+    at.split_flag = c->part_flag;
     c->launches += 1;  // the merge kernel
   }
   if (paired)
@@ -945,19 +951,26 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   for (auto& p : plan) { n_ut += ntiles(p.u_cnt); n_st += ntiles(p.sel_cnt); }
   // small grids (e.g. one request's selected rows) fill the SMs badly: split the KV range of every
   // query tile over several CTAs and merge (tcgen05 kernel only); every entry repeats per split
-  if (prm->attn_kernel < RC_ATTN_AUTO || prm->attn_kernel > RC_ATTN_SPLIT2)
+  if (prm->attn_kernel < RC_ATTN_AUTO || prm->attn_kernel > RC_ATTN_ADAPTIVE)
     return fail(RC_E_INVALID, "attn_kernel must be one of RC_ATTN_*");
   const int ak = c->attn_tc ? prm->attn_kernel : RC_ATTN_SINGLE;
-  int split_u = 1, split_s = 1;
-  if (ak == RC_ATTN_SPLIT2) {
+  int split_u = 1, split_s = 1, smin_u = 0, smin_s = 0;
+  if (ak == RC_ATTN_SPLIT2 || ak == RC_ATTN_ADAPTIVE) {
     split_u = mass ? 1 : 2;
     split_s = 2;
+    if (ak == RC_ATTN_ADAPTIVE) {  // split only tiles reaching half the longest prompt's KV tiles
+      int nmax = 0;
+      for (auto& p : plan) nmax = std::max(nmax, p.sq->n);
+      smin_s = std::max(2, (nmax + 127) / 128 / 2);
+      smin_u = mass ? 0 : smin_s;
+    }
   } else if (ak == RC_ATTN_AUTO && c->attn_tc) {
     int64_t ntok = 0;
     for (auto& p : plan) ntok += p.sq->n;
     const int est_kv = static_cast<int>(ntok / n_req / 128) + 1;
-    split_u = mass ? 1 : attn_tc_choose_splits(n_ut, m.n_kv_heads, est_kv, c->num_sms);  // mass: U tiles feed pass 1
-    split_s = attn_tc_choose_splits(n_st, m.n_kv_heads, est_kv, c->num_sms);
+    split_u = mass ? 1 : attn_tc_choose_splits(n_ut, m.n_kv_heads, est_kv, c->num_sms, &smin_u);  // mass: U tiles feed pass 1
+    if (mass) smin_u = 0;
+    split_s = attn_tc_choose_splits(n_st, m.n_kv_heads, est_kv, c->num_sms, &smin_s);
   }
   // large grids: two query tiles of one request per CTA share every K/V tile load (k_attn_pair.cu);
   // a request's odd tile count is padded with one empty tile
@@ -1046,7 +1059,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   attn_u *= 4.0 * m.n_heads * m.head_dim;
   const int pend_idx = c->prof ? static_cast<int>(c->pend.size()) : -1;
   for (int l = 0; l < cL; ++l) {
-    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, pair_u, attn_u, -1, s);
+    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, smin_u, pair_u, attn_u, -1, s);
     if (st != RC_OK) return st;
   }
   // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
@@ -1089,7 +1102,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
             gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
   // ---- a5-a7: selective layers c..L-1 on Sel
   for (int l = cL; l < L; ++l) {
-    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, pair_s, 0.0, pend_idx, s);
+    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, smin_s, pair_s, 0.0, pend_idx, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout

@@ -102,13 +102,15 @@ struct AttnArgs {
   float* part_o = nullptr;   // [n_tiles][Hk][128][128]
   float* part_ml = nullptr;  // [n_tiles][Hk][128][2]
   float* lse_out = nullptr;  // optional [R][H]: m + log2(l) per query row (k_attn_tc, n_splits = 1; NEXT-1)
+  int32_t split_min = 0;     // > 0 with n_splits = 2: adaptive split (tiles under split_min KV tiles unsplit)
+  int32_t* split_flag = nullptr;  // [n_tiles / n_splits][Hk]: 1 = the tile was split (adaptive mode)
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
 // tcgen05 version (head_dim == 128): 128-row tiles, Q via a 3-D tensor map over q [R][H][dh],
 // K/V via 2-D maps over the layer's arena [Hk*T_cap][dh] (k_attn_tc.cu)
 int attn_tc_tokens_per_tile(int group);
-int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms);
+int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms, int* split_min);
 cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV, const AttnArgs& a,
                            int64_t t_cap, cudaStream_t s);
 // paired-tile version for large grids (k_attn_pair.cu): a.tiles holds 2 entries per CTA, both of one
