@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines, no oracle)")
+    ap.add_argument("--host-frac", type=float, default=0.0,
+                    help="NEXT-2: this fraction of the catalog lives only in the pinned host tier; each batch's "
+                         "host-tier candidates are pulled by rc_fetch_host on a side stream during the previous batch")
     return ap.parse_args()
 
 
@@ -114,7 +117,7 @@ def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
                 routed=[int((routes == p).sum()) for p in range(world)])
 
 
-def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None):
+def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_frac=0.0):
     import torch
     import rcgen
     from paper_2605_07443_b200.api import RcContext
@@ -133,11 +136,21 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None):
         reqs = rcgen.gen_requests(wl, cat, protos, batch * n_batches, start=rank * 1_000_000)
         items = list(range(wl.n_items))
         remote_rows = 0
+    host_items = []
+    if host_frac > 0:  # NEXT-2: a seeded (1 - host_frac) share of the catalog stays in HBM, the rest in host DRAM
+        rng = np.random.default_rng(7)
+        on_host = set(rng.choice(items, int(round(host_frac * len(items))), replace=False).tolist())
+        host_items = [i for i in items if i in on_host]
+        items = [i for i in items if i not in on_host]
+        per_batch = max(len({int(i) for r in reqs[b * batch:(b + 1) * batch] for i in r.cand_items} & on_host)
+                        for b in range(n_batches))
+        remote_rows += per_batch * wl.item_len
     used_protos = sorted({int(p) for r in reqs for p in r.hist_protos})
     n = wl.n
     ctx = RcContext(shape, W, item_rows=len(items) * wl.item_len + remote_rows, hist_rows=wl.n_protos,
                     prefix_rows=wl.prefix_len, arena_rows=batch * n, max_seq_len=n, max_batch_tokens=batch * n,
-                    remote_rows=remote_rows, device=device.index or 0)
+                    remote_rows=remote_rows, device=device.index or 0,
+                    host_item_rows=len(host_items) * wl.item_len)
     # item pool: this GPU's items (whole catalog at N=1), generated on the device in chunks and registered
     chunk = 128
     for i0 in range(0, len(items), chunk):
@@ -145,6 +158,12 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None):
         kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
         ctx.pool_register_blocks(R.RC_POOL_ITEM_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids),
                                  kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
+        del kv
+    for i0 in range(0, len(host_items), chunk):  # NEXT-2 host tier (pinned DRAM, written over PCIe)
+        ids = host_items[i0:i0 + chunk]
+        kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
+        ctx.pool_register_blocks(R.RC_POOL_ITEM_HOST_BF16, ids, [wl.item_len] * len(ids),
+                                 [wl.prefix_len] * len(ids), kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
         del kv
     for i0 in range(0, len(used_protos), 4096):
         ids = used_protos[i0:i0 + 4096]
@@ -167,8 +186,13 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None):
         fetch = [cluster.plan_fetch([r.cand_items for r in reqs[b * batch:(b + 1) * batch]], shard["res"][rank],
                                     directory, rank) for b in range(n_batches)]
         shard["fetch_items_per_batch"] = float(np.mean([len(f) for f in fetch]))
+    host_fetch = None
+    if host_items:
+        hs = set(host_items)
+        host_fetch = [sorted({int(i) for r in reqs[b * batch:(b + 1) * batch] for i in r.cand_items} & hs)
+                      for b in range(n_batches)]
     return dict(ctx=ctx, W=W, cat=cat, protos=protos, sys=sys_tok, reqs=reqs, batches=batches, shape=shape,
-                shard=shard, fetch=fetch)
+                shard=shard, fetch=fetch, host_fetch=host_fetch)
 
 
 def host_bytes(batch_layouts):
@@ -346,12 +370,26 @@ def run_ours(args, wl):
         dist.all_gather_object(lst, obj)
         return lst
 
-    env = build_ours(wl, batch, args.distinct_batches, rank, device, world=world, gather=gather)
+    env = build_ours(wl, batch, args.distinct_batches, rank, device, world=world, gather=gather,
+                     host_frac=args.host_frac)
     ctx, batches, fetch = env["ctx"], env["batches"], env["fetch"]
     n_cand = sum(len(l["cand_idtok"]) for l in batches[0])
     out_bufs = {"logits": torch.empty((batch, wl.shape.vocab), dtype=torch.float32, device=device),
                 "cand_scores": torch.empty((n_cand,), dtype=torch.float32, device=device)}
     stream = torch.cuda.current_stream(device)
+
+    host_fetch = env["host_fetch"]
+    side = torch.cuda.Stream(device) if host_fetch else None
+    hf = {"ev": {}, "t": []}  # NEXT-2: per batch index, the event its host-tier fetch completes on
+
+    def fetch_host(i):  # issued on the side stream; the copy engines overlap the main stream's kernels
+        b = i % len(batches)
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(side)
+        ctx.fetch_host(host_fetch[b], stream=side)
+        e.record(side)
+        hf["ev"][i] = e
+        hf["t"].append((a, e))
 
     def step(i, out=out_bufs):
         b = i % len(batches)
@@ -360,7 +398,14 @@ def run_ours(args, wl):
             f = fetch[b]
             ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], [x[2] for x in f], [wl.item_len] * len(f),
                              [wl.prefix_len] * len(f), stream=stream)
+        if host_fetch:
+            if i not in hf["ev"]:
+                fetch_host(i)
+            stream.wait_event(hf["ev"].pop(i))
         seqs = ctx.assemble(lay, prefix_id=1, gather_from=c, stream=stream)
+        if host_fetch:  # batch i+1's host-tier items, after batch i's gather has read the remote region
+            side.wait_stream(stream)
+            fetch_host(i + 1)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
                               out=out, stream=stream)
         ctx.release(seqs)
@@ -461,6 +506,15 @@ def run_ours(args, wl):
            "kernels": kern, "gpu_launches": int(launches), "clocks": cl,
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_bytes(batches[0]),
                    "d2h_bytes_per_step": int(pin_l.numel() * 4 + pin_c.numel() * 4)}}
+    if host_fetch:
+        torch.cuda.synchronize(device)
+        ts = [a.elapsed_time(e) for a, e in hf["t"][-args.steps:]]
+        nb = float(np.mean([len(h) for h in host_fetch])) * wl.item_len * wl.shape.n_layers * 2 * \
+            wl.shape.n_kv_heads * wl.shape.head_dim * 2
+        res["host_tier"] = {"host_frac": args.host_frac, "items_per_batch": float(np.mean([len(h) for h in host_fetch])),
+                            "bytes_per_batch": nb, "h2d_ms_per_batch": float(np.median(ts)),
+                            "h2d_gbs": nb / (float(np.median(ts)) / 1e3) / 1e9,
+                            "note": "rc_fetch_host of batch i+1 on a side stream (copy engines) during batch i"}
     if env["shard"] is not None:
         sh = env["shard"]
         res["shard"] = {"k": world, "edge_cut": sh["cut"], "hot_replicated": int((sh["part"] == -1).sum()),

@@ -45,7 +45,7 @@ typedef struct rc_ctx rc_ctx;
 typedef uint64_t rc_seq;     /* handle of an assembled request (its stitched KV) */
 typedef void* rc_stream;     /* cudaStream_t */
 
-enum { RC_POOL_ITEM_BF16 = 0, RC_POOL_HIST_INT8 = 1, RC_POOL_PREFIX_BF16 = 2 };
+enum { RC_POOL_ITEM_BF16 = 0, RC_POOL_HIST_INT8 = 1, RC_POOL_PREFIX_BF16 = 2, RC_POOL_ITEM_HOST_BF16 = 3 };
 enum { RC_TOK_PREFIX = 0, RC_TOK_FORCED = 1, RC_TOK_HIST = 2, RC_TOK_ITEM = 3 };
 enum { RC_MISS_ERROR = 0, RC_MISS_RECOMPUTE = 1 };
 
@@ -88,6 +88,9 @@ typedef struct rc_pool_desc {
   int64_t arena_rows;       /* stitched-KV arena tokens (sum of live padded requests)       */
   int32_t max_seq_len;      /* longest prompt; <= 8192 (R6 key packing)                      */
   int32_t max_batch_tokens; /* largest sum of n in one rc_selective_prefill call            */
+  int64_t host_item_rows;   /* host-tier item pool tokens (pinned host DRAM, same layout;
+                               NEXT-2); 0 = none. Blocks there become resident in HBM only
+                               through rc_fetch_host                                          */
 } rc_pool_desc;
 
 /* One request in decomposed form (output of rc_decompose_prompt; host memory). */
@@ -243,6 +246,16 @@ rc_status rc_peer_attach(rc_ctx* ctx, int32_t n_peers, const int32_t* peer_rank,
 rc_status rc_fetch_remote(rc_ctx* ctx, int32_t n_items, const uint64_t* item_ids, const int32_t* owner_rank,
                           const int64_t* owner_row, const int32_t* n_tokens, const int32_t* canon_pos,
                           rc_stream stream);
+/* Host tier (the paper's CPU-resident item cache with its PCIe transfer,
+ * PAPER.md:551, 566): copy item blocks registered with RC_POOL_ITEM_HOST_BF16 into this
+ * context's remote-cache region (LRU, shared with rc_fetch_remote) with the copy engines (one
+ * 2-D H2D copy per block: L*2*H_kv runs of n_tokens*d_h*2 bytes), so the transfer uses no SMs and
+ * overlaps kernels when issued on a side stream -- e.g. the next batch's host-tier items while
+ * the current batch computes. Already-resident ids are skipped. Ordering: a fetch may evict
+ * remote blocks that are not part of this call; the caller orders it after the rc_assemble that
+ * read them (stream or event). Errors: NOTFOUND (id in no tier), CAPACITY (remote region too
+ * small for one call), INVALID (no host tier). */
+rc_status rc_fetch_host(rc_ctx* ctx, int32_t n_items, const uint64_t* item_ids, rc_stream stream);
 /* First pool row of resident item blocks (-1 if absent), for building fetch requests. */
 rc_status rc_pool_locate(rc_ctx* ctx, int32_t n, const uint64_t* item_ids, int64_t* rows_out);
 

@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(HERE, "librc.so")
 
 RC_OK, RC_E_INVALID, RC_E_NOMEM, RC_E_CAPACITY, RC_E_NOTFOUND, RC_E_EXISTS, RC_E_CUDA, RC_E_PEER, RC_E_UNSUPPORTED = \
     0, -1, -2, -3, -4, -5, -6, -7, -8
-RC_POOL_ITEM_BF16, RC_POOL_HIST_INT8, RC_POOL_PREFIX_BF16 = 0, 1, 2
+RC_POOL_ITEM_BF16, RC_POOL_HIST_INT8, RC_POOL_PREFIX_BF16, RC_POOL_ITEM_HOST_BF16 = 0, 1, 2, 3
 RC_TOK_PREFIX, RC_TOK_FORCED, RC_TOK_HIST, RC_TOK_ITEM = 0, 1, 2, 3
 RC_MISS_ERROR, RC_MISS_RECOMPUTE = 0, 1
 
@@ -38,7 +38,7 @@ class Weights(C.Structure):
 class PoolDesc(C.Structure):
     _fields_ = [("item_rows", C.c_int64), ("remote_rows", C.c_int64), ("hist_rows", C.c_int64),
                 ("prefix_rows", C.c_int64), ("arena_rows", C.c_int64), ("max_seq_len", C.c_int32),
-                ("max_batch_tokens", C.c_int32)]
+                ("max_batch_tokens", C.c_int32), ("host_item_rows", C.c_int64)]
 
 
 class Request(C.Structure):
@@ -93,6 +93,7 @@ def lib():
             "rc_pool_export": (C.c_int32, [P, P, I64P]),
             "rc_peer_attach": (C.c_int32, [P, C.c_int32, I32P, I32P, PP, I64P]),
             "rc_fetch_remote": (C.c_int32, [P, C.c_int32, U64P, I32P, I64P, I32P, I32P, P]),
+            "rc_fetch_host": (C.c_int32, [P, C.c_int32, U64P, P]),
             "rc_seq_read_kv": (C.c_int32, [P, C.c_uint64, C.c_int32, P, P, P]),
             "rc_diag_deviation_select": (C.c_int32, [C.c_int32, C.c_int32, P, P, P, P, U8P, C.c_int32, C.c_int32,
                                                      C.c_int32, C.c_int32, P, P, I32P, P]),
@@ -128,5 +129,5 @@ EXPORTED = ["rc_create", "rc_destroy", "rc_last_error", "rc_abi_version", "rc_de
             "rc_pool_register_blocks", "rc_pool_contains", "rc_pool_locate", "rc_assemble", "rc_sel_count",
             "rc_selective_prefill", "rc_release", "rc_pool_export", "rc_peer_attach", "rc_fetch_remote",
             "rc_seq_read_kv", "rc_diag_deviation_select", "rc_diag_gemm", "rc_launch_count", "rc_profile_begin",
-            "rc_profile_end", "rc_place_items", "rc_route"]
+            "rc_profile_end", "rc_place_items", "rc_route", "rc_fetch_host"]
 KINDS = ["gemm", "attention", "gather", "select", "small", "lm_head", "fetch"]

@@ -31,7 +31,7 @@ class RcContext:
     """rc_create/rc_destroy around one device. `weights`: rcgen naming, bf16 CUDA tensors."""
 
     def __init__(self, shape, weights, item_rows, hist_rows, prefix_rows, arena_rows, max_seq_len, max_batch_tokens,
-                 remote_rows=0, device=0):
+                 remote_rows=0, device=0, host_item_rows=0):
         lib()
         self.shape = shape
         self.device = device
@@ -44,7 +44,8 @@ class RcContext:
             p, arr = _ptr_array([lw[name] for lw in weights["layers"]])
             self._keep.append(arr)
             setattr(w, name, p)
-        pd = R.PoolDesc(item_rows, remote_rows, hist_rows, prefix_rows, arena_rows, max_seq_len, max_batch_tokens)
+        pd = R.PoolDesc(item_rows, remote_rows, hist_rows, prefix_rows, arena_rows, max_seq_len, max_batch_tokens,
+                        host_item_rows)
         out = C.c_void_p()
         check(lib().rc_create(C.byref(md), C.byref(w), C.byref(pd), device, C.byref(out)))
         self.ctx = out
@@ -225,6 +226,12 @@ class RcContext:
         check(lib().rc_fetch_remote(self.ctx, len(ids), np_ptr(ids, C.c_uint64), np_ptr(o, C.c_int32),
                                     np_ptr(orow, C.c_int64), np_ptr(nt, C.c_int32), np_ptr(cp, C.c_int32),
                                     _stream(stream)))
+
+
+    def fetch_host(self, item_ids, stream=None):
+        """rc_fetch_host: host-tier item blocks -> the HBM remote-cache region on the copy engines."""
+        ids = np.ascontiguousarray(item_ids, np.uint64)
+        check(lib().rc_fetch_host(self.ctx, len(ids), np_ptr(ids, C.c_uint64), _stream(stream)))
 
 
 def diag_gemm(A, B, bn=256, stream=None):

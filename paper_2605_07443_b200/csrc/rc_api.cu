@@ -183,6 +183,11 @@ struct rc_ctx {
   RangeAlloc item_alloc, remote_alloc;
   int64_t hist_used = 0, prefix_used = 0;
   std::unordered_map<uint64_t, Block> items, protos, prefixes;
+  // NEXT-2 host tier: pinned, mapped host DRAM in the pool layout [L][2][Hk][host_rows][dh]
+  uint16_t* host_pool = nullptr;      // host pointer
+  uint16_t* host_pool_dev = nullptr;  // its device mapping (registration writes)
+  int64_t host_used = 0;
+  std::unordered_map<uint64_t, Block> host_items;
   uint64_t use_clock = 1;
   // peers
   std::unordered_map<int, std::pair<const uint16_t*, int64_t>> peers;  // rank -> (pool base, rows)
@@ -253,6 +258,7 @@ struct rc_ctx {
                     mass_lse, mass_a};
     for (void* p : bufs)
       if (p) cudaFree(p);
+    if (host_pool) cudaFreeHost(host_pool);
   }
 };
 
@@ -396,6 +402,17 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
     c->prefix_pool = dev_alloc<uint16_t>(static_cast<size_t>(planes) * pd->prefix_rows * dh, &e);
     if (e != cudaSuccess) return fail(RC_E_NOMEM, "prefix pool");
   }
+  if (pd->host_item_rows < 0) return fail(RC_E_INVALID, "negative host_item_rows");
+  if (pd->host_item_rows > 0) {  // NEXT-2: pinned + mapped host tier
+    const size_t bytes = static_cast<size_t>(planes) * pd->host_item_rows * dh * 2;
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, bytes, cudaHostAllocMapped) != cudaSuccess)
+      return fail(RC_E_NOMEM, "host-tier item pool (pinned)");
+    c->host_pool = static_cast<uint16_t*>(hp);
+    void* dp = nullptr;
+    RC_CUDA(cudaHostGetDevicePointer(&dp, hp, 0));
+    c->host_pool_dev = static_cast<uint16_t*>(dp);
+  }
   c->arena = dev_alloc<uint16_t>(static_cast<size_t>(planes) * std::max<int64_t>(pd->arena_rows, 1) * dh, &e);
   if (e != cudaSuccess) return fail(RC_E_NOMEM, "stitched-KV arena");
   // every arena byte stays a finite bf16 (attention tiles may read rows past a request's end; they are
@@ -505,7 +522,8 @@ rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, con
   RC_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   auto* dir = kind == RC_POOL_ITEM_BF16 ? &c->items : kind == RC_POOL_HIST_INT8 ? &c->protos
-              : kind == RC_POOL_PREFIX_BF16 ? &c->prefixes : nullptr;
+              : kind == RC_POOL_PREFIX_BF16 ? &c->prefixes : kind == RC_POOL_ITEM_HOST_BF16 ? &c->host_items
+              : nullptr;
   if (!dir) return fail(RC_E_INVALID, "unknown pool kind");
   if (kind == RC_POOL_HIST_INT8 && !scales) return fail(RC_E_INVALID, "history blocks need scales");
   int64_t total = 0;
@@ -524,6 +542,11 @@ rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, con
     row0 = c->item_alloc.alloc(total);
     if (row0 < 0) return fail(RC_E_CAPACITY, "item pool full");
     rows_cap = c->pd.item_rows;
+  } else if (kind == RC_POOL_ITEM_HOST_BF16) {
+    if (!c->host_pool) return fail(RC_E_INVALID, "no host tier (host_item_rows = 0)");
+    if (c->host_used + total > c->pd.host_item_rows) return fail(RC_E_CAPACITY, "host-tier item pool full");
+    row0 = c->host_used;
+    rows_cap = c->pd.host_item_rows;
   } else if (kind == RC_POOL_HIST_INT8) {
     if (c->hist_used + total > c->pd.hist_rows) return fail(RC_E_CAPACITY, "history pool full");
     row0 = c->hist_used;
@@ -541,7 +564,9 @@ rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, con
     c->launches += 2;  // offline registration: counted, never profiled
   } else {
     e = pool_transpose_launch(kv, 2, static_cast<int32_t>(total), L, Hk, dh,
-                              kind == RC_POOL_ITEM_BF16 ? c->item_pool : c->prefix_pool, rows_cap, row0, s);
+                              kind == RC_POOL_ITEM_BF16 ? c->item_pool
+                              : kind == RC_POOL_ITEM_HOST_BF16 ? c->host_pool_dev : c->prefix_pool,
+                              rows_cap, row0, s);
     c->launches += 1;
   }
   if (e != cudaSuccess) {
@@ -555,13 +580,15 @@ rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, con
   }
   if (kind == RC_POOL_HIST_INT8) c->hist_used += total;
   if (kind == RC_POOL_PREFIX_BF16) c->prefix_used += total;
+  if (kind == RC_POOL_ITEM_HOST_BF16) c->host_used += total;
   return RC_OK;
 }
 
 rc_status rc_pool_contains(rc_ctx* c, int32_t kind, int32_t n, const uint64_t* ids, uint8_t* out) {
   if (!c || (n > 0 && (!ids || !out))) return fail(RC_E_INVALID, "null argument");
   auto* dir = kind == RC_POOL_ITEM_BF16 ? &c->items : kind == RC_POOL_HIST_INT8 ? &c->protos
-              : kind == RC_POOL_PREFIX_BF16 ? &c->prefixes : nullptr;
+              : kind == RC_POOL_PREFIX_BF16 ? &c->prefixes : kind == RC_POOL_ITEM_HOST_BF16 ? &c->host_items
+              : nullptr;
   if (!dir) return fail(RC_E_INVALID, "unknown pool kind");
   for (int i = 0; i < n; ++i) out[i] = dir->count(ids[i]) ? 1 : 0;
   return RC_OK;
@@ -1228,6 +1255,49 @@ rc_status rc_fetch_remote(rc_ctx* c, int32_t n_items, const uint64_t* ids, const
               copy_rows_launch(peer.first, peer.second, owner_row[i], c->item_pool, c->pd.item_rows, grow, n_tokens[i],
                                static_cast<int32_t>(planes), row_bytes, s));
     c->items[ids[i]] = Block{grow, n_tokens[i], canon_pos[i], true, c->use_clock};
+  }
+  return RC_OK;
+}
+
+rc_status rc_fetch_host(rc_ctx* c, int32_t n_items, const uint64_t* ids, rc_stream stream) {
+  if (!c || n_items < 0 || (n_items > 0 && !ids)) return fail(RC_E_INVALID, "null argument");
+  if (!c->host_pool) return fail(RC_E_INVALID, "no host tier (host_item_rows = 0)");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t need = 0;
+  ++c->use_clock;  // blocks of this call are protected from eviction by it
+  for (int i = 0; i < n_items; ++i) {
+    if (c->items.count(ids[i])) { c->items[ids[i]].last_use = c->use_clock; continue; }
+    auto it = c->host_items.find(ids[i]);
+    if (it == c->host_items.end()) return fail(RC_E_NOTFOUND, "item " + std::to_string(ids[i]) + " in no tier");
+    need += it->second.n;
+  }
+  if (need > c->pd.remote_rows) return fail(RC_E_CAPACITY, "remote region smaller than one host fetch");
+  const int64_t planes = plane_count(c);
+  const size_t row_bytes = static_cast<size_t>(c->m.head_dim) * 2;
+  for (int i = 0; i < n_items; ++i) {
+    if (c->items.count(ids[i])) continue;
+    const Block hb = c->host_items[ids[i]];
+    int64_t row = c->remote_alloc.alloc(hb.n);
+    while (row < 0) {  // evict least-recently used remote blocks not used by this call
+      uint64_t victim = 0, best = ~0ull;
+      for (auto& kv : c->items)
+        if (kv.second.remote && kv.second.last_use < best && kv.second.last_use != c->use_clock) {
+          best = kv.second.last_use;
+          victim = kv.first;
+        }
+      if (best == ~0ull) return fail(RC_E_CAPACITY, "remote region exhausted");
+      const Block b = c->items[victim];
+      c->remote_alloc.release(b.row - (c->pd.item_rows - c->pd.remote_rows), b.n);
+      c->items.erase(victim);
+      row = c->remote_alloc.alloc(hb.n);
+    }
+    const int64_t grow = (c->pd.item_rows - c->pd.remote_rows) + row;
+    // one 2-D copy on the copy engines: `planes` runs of n rows, pitches = the two pools' plane strides
+    RC_CUDA(cudaMemcpy2DAsync(c->item_pool + grow * c->m.head_dim, c->pd.item_rows * row_bytes,
+                              c->host_pool + hb.row * c->m.head_dim, c->pd.host_item_rows * row_bytes,
+                              hb.n * row_bytes, planes, cudaMemcpyHostToDevice, s));
+    c->items[ids[i]] = Block{grow, hb.n, hb.canon, true, c->use_clock};
   }
   return RC_OK;
 }

@@ -75,6 +75,46 @@ def test_gather_bitexact(wl, gather_from):
     ctx.close()
 
 
+def test_host_tier_fetch_then_gather_bitexact():
+    """NEXT-2 host tier: item blocks registered only in pinned host DRAM, pulled into the HBM
+    remote-cache region by rc_fetch_host on a side stream (copy engines), then gathered: the
+    stitched KV equals O-ASM bit for bit, and a second fetch of the same ids is a no-op."""
+    from paper_2605_07443_b200.api import RcContext
+    from paper_2605_07443_b200 import _lib as R
+    G = _gpu()
+    wl = rcgen.MINI_L
+    case = make_case(wl, n_req=2)
+    pools = oracle_pools(case)
+    shape = case["shape"]
+    L, Hk, dh = shape.n_layers, shape.n_kv_heads, shape.head_dim
+    ids = pools["item_ids"]
+    rows = len(ids) * wl.item_len
+    Wd = G.weights_to(case["W"])
+    ctx = RcContext(shape, Wd, item_rows=rows, remote_rows=rows, hist_rows=len(pools["proto_ids"]),
+                    prefix_rows=wl.prefix_len, arena_rows=2 * wl.n, max_seq_len=max(wl.n, 256),
+                    max_batch_tokens=2 * wl.n, host_item_rows=rows)
+    kv = pools["item_kv"].reshape(rows, L, 2, Hk, dh).contiguous().cuda()
+    ctx.pool_register_blocks(R.RC_POOL_ITEM_HOST_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids), kv)
+    G.register_pools(ctx, case, pools, items=[])
+    assert not ctx.pool_contains(R.RC_POOL_ITEM_BF16, ids).any() and ctx.pool_contains(R.RC_POOL_ITEM_HOST_BF16, ids).all()
+    side = torch.cuda.Stream()
+    ctx.fetch_host(ids, stream=side)
+    ctx.fetch_host(ids, stream=side)  # resident now: skipped
+    torch.cuda.current_stream().wait_stream(side)
+    assert ctx.pool_contains(R.RC_POOL_ITEM_BF16, ids).all()
+    lays = G.gpu_layouts(ctx, case)
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=1)
+    torch.cuda.synchronize()
+    for r, lay in enumerate(layouts(case)):
+        K, V, dfn = assemble(shape, lay, pools["items"], pools["hist"], pools["prefix"], 1)
+        for l in range(1, L):
+            k, v = ctx.read_kv(seqs[r], l, lay.n)
+            m = dfn[l]
+            assert np.array_equal(G.bits(k)[m], K[l][m]) and np.array_equal(G.bits(v)[m], V[l][m]), l
+    ctx.release(seqs)
+    ctx.close()
+
+
 # ----------------------------------------------------------------------------- K5 + K6 unit
 @pytest.mark.parametrize("n_u,width,r_bp,window", [(136, 64, 1500, 0), (3889, 2048, 1500, 0), (2353, 2048, 500, 0),
                                                    (1000, 256, 3000, 17), (64, 32, 10000, 0), (500, 64, 0, 0)])
