@@ -353,9 +353,12 @@ def run_ours(args, wl):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RC_BENCH_SHARE_GPU=1 (diagnostics): run every rank on cuda:0 over gloo, to exercise the N > 1 code
+    # path (placement, routing, IPC peer mapping, NVLink-style fetch) on a one-GPU box
+    share = os.environ.get("RC_BENCH_SHARE_GPU") == "1"
     if world > 1:
-        dist.init_process_group("nccl")
-    device = torch.device("cuda", local)
+        dist.init_process_group("gloo" if share else "nccl")
+    device = torch.device("cuda", 0 if share else local)
     torch.cuda.set_device(device)
     from paper_2605_07443_b200.build import build
     if rank == 0:
@@ -430,7 +433,7 @@ def run_ours(args, wl):
     if world > 1:
         dist.barrier()
     cl = clocks.stop() if clocks else None
-    t = torch.tensor([total_ms], device=device)
+    t = torch.tensor([total_ms], device="cpu" if share else device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
@@ -458,7 +461,7 @@ def run_ours(args, wl):
         pin_c.copy_(out_bufs["cand_scores"], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize(device)
-    te = torch.tensor([max(e0.elapsed_time(e1), 1e-6)], device=device)
+    te = torch.tensor([max(e0.elapsed_time(e1), 1e-6)], device="cpu" if share else device)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = tokens_all / (float(te.item()) / 1e3)

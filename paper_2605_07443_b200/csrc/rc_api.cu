@@ -1202,7 +1202,7 @@ rc_status rc_peer_attach(rc_ctx* c, int32_t n, const int32_t* rank, const int32_
       c->peers[rank[i]] = {c->item_pool, c->pd.item_rows};  // loopback
       continue;
     }
-    if (peer_dev) {
+    if (peer_dev && peer_dev[i] != c->device) {  // another process on this same device needs no P2P path
       int can = 0;
       cudaDeviceCanAccessPeer(&can, c->device, peer_dev[i]);
       if (!can) return fail(RC_E_PEER, "no P2P path to peer device " + std::to_string(peer_dev[i]));
