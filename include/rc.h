@@ -259,6 +259,23 @@ rc_status rc_fetch_host(rc_ctx* ctx, int32_t n_items, const uint64_t* item_ids, 
 /* First pool row of resident item blocks (-1 if absent), for building fetch requests. */
 rc_status rc_pool_locate(rc_ctx* ctx, int32_t n, const uint64_t* item_ids, int64_t* rows_out);
 
+/* ---------------------------------------------------------------- semantic library (NEXT-3) */
+/* Online LSH matching of history tokens to prototypes (SPEC.md:237-263
+ * embed_token / match_token) under DESIGN.md reading R-LSH: position-aware unit embeddings of
+ * D = 64 (48 seeded feature-hash lexical dims + 16 sinusoidal dims of the log2 bucket of the
+ * history offset), 8 tables x 16-bit random-hyperplane signatures, fixed fp32 reduction order.
+ * Build (host arrays, copied): prototype pi = (proto_token[pi], proto_offset[pi]) with centroid
+ * embed(token, offset); hyperplanes fp32 [128][64] (table-major); replaces any earlier library.
+ * Errors: INVALID (n_proto <= 0, n_buckets not in [1, 32], negative offset), NOMEM. */
+rc_status rc_semlib_build(rc_ctx* ctx, int32_t n_proto, const int32_t* proto_token, const int32_t* proto_offset,
+                          int32_t n_buckets, const float* hyperplanes, uint64_t seed);
+/* Match n history tokens (DEVICE int32 token ids and history offsets) -> DEVICE proto_out int32
+ * [n] (max-cosine prototype over the union of the 8 LSH buckets, ties -> smaller id; no candidate
+ * -> best of the query's log bucket, else of all prototypes) and cos_out f32 [n]. Async on
+ * `stream`. Errors: INVALID (no library, null pointers). */
+rc_status rc_semlib_match(rc_ctx* ctx, int32_t n, const int32_t* token, const int32_t* offset, int32_t* proto_out,
+                          float* cos_out, rc_stream stream);
+
 /* ---------------------------------------------------------------- profiling */
 /* Kernel classes for per-kind timing. */
 enum { RC_K_GEMM = 0, RC_K_ATTN = 1, RC_K_GATHER = 2, RC_K_SELECT = 3, RC_K_SMALL = 4, RC_K_LMHEAD = 5,

@@ -234,6 +234,24 @@ class RcContext:
         check(lib().rc_fetch_host(self.ctx, len(ids), np_ptr(ids, C.c_uint64), _stream(stream)))
 
 
+    def semlib_build(self, proto_token, proto_offset, n_buckets, hyperplanes, seed):
+        """rc_semlib_build (NEXT-3): host arrays; hyperplanes float32 [128][64]."""
+        tok = np.ascontiguousarray(proto_token, np.int32)
+        off = np.ascontiguousarray(proto_offset, np.int32)
+        H = np.ascontiguousarray(hyperplanes, np.float32)
+        check(lib().rc_semlib_build(self.ctx, len(tok), np_ptr(tok, C.c_int32), np_ptr(off, C.c_int32), int(n_buckets),
+                                    np_ptr(H, C.c_float), int(seed)))
+
+    def semlib_match(self, token, offset, stream=None):
+        """rc_semlib_match: CUDA int32 tensors -> (proto ids int32, cosines float32) CUDA tensors."""
+        n = token.numel()
+        dev = torch.device("cuda", self.device)
+        pid = torch.empty(n, dtype=torch.int32, device=dev)
+        cos = torch.empty(n, dtype=torch.float32, device=dev)
+        check(lib().rc_semlib_match(self.ctx, n, _dptr(token), _dptr(offset), _dptr(pid), _dptr(cos), _stream(stream)))
+        return pid, cos
+
+
 def diag_gemm(A, B, bn=256, stream=None):
     M, K = A.shape
     N = B.shape[0]

@@ -16,7 +16,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr", "-Xptxas", "-v",
          "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["rc_api.cu", "rc_place.cu", "k_gemm.cu", "k_gather.cu", "k_attn.cu", "k_attn_tc.cu", "k_attn_pair.cu", "k_attn_mass.cu", "k_small.cu"]
+SOURCES = ["rc_api.cu", "rc_place.cu", "k_gemm.cu", "k_gather.cu", "k_attn.cu", "k_attn_tc.cu", "k_attn_pair.cu", "k_attn_mass.cu", "k_semlib.cu", "k_small.cu"]
 
 
 def _stale(obj, src):

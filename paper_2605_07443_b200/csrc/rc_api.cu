@@ -234,6 +234,9 @@ struct rc_ctx {
   float* mass_lse = nullptr;
   unsigned long long* mass_a = nullptr;
   CUtensorMap mK_mass{}, mV_mass{};
+  // NEXT-3 semantic library (device arrays, owned)
+  SemlibArgs semlib{};
+  std::vector<void*> semlib_bufs;
   int attn_tq() const { return attn_tc ? attn_tc_tokens_per_tile(m.n_heads / m.n_kv_heads)
                                        : attn_tokens_per_tile(m.n_heads / m.n_kv_heads); }
   int bn_qkv = 256, bn_kv = 256, bn_o = 256, bn_d = 256, bn_lm = 256;
@@ -259,6 +262,7 @@ struct rc_ctx {
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
+    for (void* p : semlib_bufs) cudaFree(p);
   }
 };
 
@@ -1299,6 +1303,89 @@ rc_status rc_fetch_host(rc_ctx* c, int32_t n_items, const uint64_t* ids, rc_stre
                               hb.n * row_bytes, planes, cudaMemcpyHostToDevice, s));
     c->items[ids[i]] = Block{grow, hb.n, hb.canon, true, c->use_clock};
   }
+  return RC_OK;
+}
+
+// ------------------------------------------------------------------ NEXT-3 semantic library
+rc_status rc_semlib_build(rc_ctx* c, int32_t n, const int32_t* tok, const int32_t* off, int32_t n_buckets,
+                          const float* H, uint64_t seed) {
+  if (!c || n <= 0 || !tok || !off || !H) return fail(RC_E_INVALID, "null argument / empty library");
+  if (n_buckets < 1 || n_buckets > 32) return fail(RC_E_INVALID, "n_buckets must be in [1, 32]");
+  for (int i = 0; i < n; ++i)
+    if (off[i] < 0) return fail(RC_E_INVALID, "negative history offset");
+  RC_CUDA(cudaSetDevice(c->device));
+  for (void* p : c->semlib_bufs) cudaFree(p);
+  c->semlib_bufs.clear();
+  c->semlib = SemlibArgs{};
+  constexpr int T = 8, D = 64;
+  cudaError_t e = cudaSuccess;
+  auto dalloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) c->semlib_bufs.push_back(p);
+    return p;
+  };
+  // positional codes: sin/cos(b 10000^(-k/8)) in fp64 by the C library, rounded once to fp32 (R-LSH)
+  std::vector<float> pos(static_cast<size_t>(n_buckets) * 16);
+  for (int b = 0; b < n_buckets; ++b)
+    for (int k = 0; k < 8; ++k) {
+      const double w = std::pow(10000.0, -static_cast<double>(k) / 8.0);
+      pos[b * 16 + 2 * k] = static_cast<float>(std::sin(b * w));
+      pos[b * 16 + 2 * k + 1] = static_cast<float>(std::cos(b * w));
+    }
+  auto* d_pos = static_cast<float*>(dalloc(pos.size() * 4));
+  auto* d_H = static_cast<float*>(dalloc(static_cast<size_t>(T) * 16 * D * 4));
+  auto* d_C = static_cast<float*>(dalloc(static_cast<size_t>(n) * D * 4));
+  auto* d_tok = static_cast<int32_t*>(dalloc(static_cast<size_t>(n) * 4));
+  auto* d_off = static_cast<int32_t*>(dalloc(static_cast<size_t>(n) * 4));
+  auto* d_sig = static_cast<uint32_t*>(dalloc(static_cast<size_t>(T) * n * 4));
+  auto* d_tsig = static_cast<uint32_t*>(dalloc(static_cast<size_t>(T) * n * 4));
+  auto* d_tid = static_cast<int32_t*>(dalloc(static_cast<size_t>(T) * n * 4));
+  auto* d_bid = static_cast<int32_t*>(dalloc(static_cast<size_t>(n) * 4));
+  auto* d_bst = static_cast<int32_t*>(dalloc(static_cast<size_t>(n_buckets + 1) * 4));
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "semantic library");
+  RC_CUDA(cudaMemcpy(d_pos, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(d_H, H, static_cast<size_t>(T) * 16 * D * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(d_tok, tok, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(d_off, off, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
+  SemlibArgs& sa = c->semlib;
+  sa.seed = seed; sa.n_buckets = n_buckets; sa.n_proto = n; sa.pos_table = d_pos; sa.H = d_H; sa.C = d_C;
+  cudaStream_t s = nullptr;  // offline build on the legacy stream (synchronised by the copy below)
+  RC_LAUNCH(RC_K_SMALL, 0, 0, -1, semlib_embed_launch(sa, n, d_tok, d_off, d_C, d_sig, s));
+  std::vector<uint32_t> sig(static_cast<size_t>(T) * n);
+  RC_CUDA(cudaMemcpy(sig.data(), d_sig, sig.size() * 4, cudaMemcpyDeviceToHost));  // synchronises
+  // per table: (signature, id) ascending -> the bucket map as two sorted arrays
+  std::vector<uint32_t> tsig(sig.size());
+  std::vector<int32_t> tid(sig.size());
+  std::vector<int32_t> order(n);
+  for (int t = 0; t < T; ++t) {
+    for (int i = 0; i < n; ++i) order[i] = i;
+    const uint32_t* st = sig.data() + static_cast<size_t>(t) * n;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return st[a] != st[b] ? st[a] < st[b] : a < b; });
+    for (int i = 0; i < n; ++i) { tsig[static_cast<size_t>(t) * n + i] = st[order[i]]; tid[static_cast<size_t>(t) * n + i] = order[i]; }
+  }
+  // prototypes grouped by log bucket of their offset
+  std::vector<int32_t> bst(n_buckets + 1, 0), bid(n);
+  auto lb = [&](int o) { int b = 31 - __builtin_clz(static_cast<unsigned>(o) + 1u); return b < n_buckets - 1 ? b : n_buckets - 1; };
+  for (int i = 0; i < n; ++i) ++bst[lb(off[i]) + 1];
+  for (int b = 0; b < n_buckets; ++b) bst[b + 1] += bst[b];
+  std::vector<int32_t> fill(bst.begin(), bst.end() - 1);
+  for (int i = 0; i < n; ++i) bid[fill[lb(off[i])]++] = i;
+  RC_CUDA(cudaMemcpy(d_tsig, tsig.data(), tsig.size() * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(d_tid, tid.data(), tid.size() * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(d_bid, bid.data(), bid.size() * 4, cudaMemcpyHostToDevice));
+  RC_CUDA(cudaMemcpy(d_bst, bst.data(), bst.size() * 4, cudaMemcpyHostToDevice));
+  sa.tab_sig = d_tsig; sa.tab_id = d_tid; sa.bucket_ids = d_bid; sa.bucket_start = d_bst;
+  return RC_OK;
+}
+
+rc_status rc_semlib_match(rc_ctx* c, int32_t n, const int32_t* tok, const int32_t* off, int32_t* proto_out,
+                          float* cos_out, rc_stream stream) {
+  if (!c || n < 0 || (n > 0 && (!tok || !off || !proto_out || !cos_out))) return fail(RC_E_INVALID, "null argument");
+  if (c->semlib.n_proto <= 0) return fail(RC_E_INVALID, "no semantic library (rc_semlib_build)");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RC_LAUNCH(RC_K_SMALL, 0, n * 16.0, -1, semlib_match_launch(c->semlib, n, tok, off, proto_out, cos_out, s));
   return RC_OK;
 }
 

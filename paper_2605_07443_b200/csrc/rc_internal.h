@@ -132,6 +132,22 @@ cudaError_t attn_mass_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, con
                              cudaStream_t s);
 cudaError_t mass_combine_launch(unsigned long long* dev, const unsigned long long* mass, int32_t n, double lam,
                                 cudaStream_t s);
+// NEXT-3 LSH prototype matching (k_semlib.cu)
+struct SemlibArgs {
+  unsigned long long seed = 0;
+  int32_t n_buckets = 0, n_proto = 0;
+  const float* pos_table = nullptr;  // [n_buckets][16] fp32
+  const float* H = nullptr;          // [8 * 16][64] hyperplanes
+  const float* C = nullptr;          // [n_proto][64] unit centroids
+  const uint32_t* tab_sig = nullptr; // [8][n_proto] ascending signatures per table
+  const int32_t* tab_id = nullptr;   // [8][n_proto] prototype ids in that order
+  const int32_t* bucket_ids = nullptr;    // prototype ids grouped by log bucket
+  const int32_t* bucket_start = nullptr;  // [n_buckets + 1]
+};
+cudaError_t semlib_embed_launch(const SemlibArgs& s, int n, const int32_t* tok, const int32_t* off, float* C,
+                                uint32_t* sig, cudaStream_t st);
+cudaError_t semlib_match_launch(const SemlibArgs& s, int n, const int32_t* tok, const int32_t* off, int32_t* proto_out,
+                                float* cos_out, cudaStream_t st);
 bool make_tmap_bf16_3d(CUtensorMap* map, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
                        uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2);
 

@@ -292,3 +292,36 @@ def test_attention_mass_scores_and_selection(wl, c, lam):
         assert jac >= 0.8, jac
         assert rel_l2(res["logits"][r], forced["logits"]) < TOL
         assert rel_l2(res["hidden"][res["sel_off"][r]:res["sel_off"][r + 1]], forced["x_sel"]) < TOL
+
+
+# ----------------------------------------------------------------------------- NEXT-3: LSH matching
+@pytest.mark.parametrize("wl,n_req", [(rcgen.CFG1, 4), (rcgen.CFG3, 2)])
+def test_semlib_match_bitexact(wl, n_req):
+    """GPU LSH prototype matching of the requests' history tokens
+    equals oracle/semlib.py bit for bit: prototype ids and fp32 cosines (R-LSH fixes the order)."""
+    from oracle.semlib import Library, T, B, D
+    G = _gpu()
+    case = make_case(rcgen.CFG1)  # any model: the library lives on the context, not on the model
+    pools = oracle_pools(case)
+    ctx, _ = G.make_ctx(case, pools, rcgen.CFG1.n)
+    protos = rcgen.gen_protos(wl)
+    cat = rcgen.gen_catalog(wl)
+    reqs = rcgen.gen_requests(wl, cat, protos, n_req)
+    H = np.random.default_rng(5).standard_normal((T * B, D)).astype(np.float32)
+    offs = (protos.canon_pos - wl.prefix_len).astype(np.int32)
+    ctx.semlib_build(protos.token, offs, protos.n_buckets, H, seed=11)
+    lib = Library(protos.token, offs, protos.n_buckets, H, 11)
+    tok = np.concatenate([r.hist_tokens for r in reqs]).astype(np.int32)
+    qoff = np.concatenate([np.arange(len(r.hist_tokens)) for r in reqs]).astype(np.int32)
+    # plus queries no prototype shares a bucket map with (fallback path): far-away tokens
+    tok = np.concatenate([tok, np.arange(7, 40, dtype=np.int32) * 977 % 500])
+    qoff = np.concatenate([qoff, np.arange(33, dtype=np.int32) * 19 % max(wl.hist_len, 1)])
+    pid, cos = ctx.semlib_match(torch.from_numpy(tok).cuda(), torch.from_numpy(qoff).cuda())
+    torch.cuda.synchronize()
+    pid, cos = pid.cpu().numpy(), cos.cpu().numpy()
+    for i in range(len(tok)):
+        p, c = lib.match(int(tok[i]), int(qoff[i]))
+        assert pid[i] == p and np.float32(c).view(np.uint32) == cos[i].view(np.uint32), (i, pid[i], p, cos[i], c)
+    # the generator's exact-match tokens (93%) find a prototype with their own embedding (cosine 1)
+    assert (np.abs(cos[:-33] - 1.0) < 1e-6).mean() > 0.5
+    ctx.close()
