@@ -56,7 +56,11 @@ class RcContext:
             lib().rc_destroy(self.ctx)
             self.ctx = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: module globals may already be gone
+            pass
 
     # ------------------------------------------------------------------ pools
     def pool_register_blocks(self, kind, ids, n_tokens, canon_pos, kv, scales=None, stream=None):

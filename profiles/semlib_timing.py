@@ -38,3 +38,4 @@ ms = a.elapsed_time(b) / reps
 print(json.dumps({"what": "rc_semlib_match, cfg3 batch-32 history tokens vs 1e5 prototypes", "queries": tok.numel(),
                   "prototypes": int(protos.n), "ms": ms, "queries_per_s": tok.numel() / ms * 1e3,
                   "exact_match_frac": float((cos - 1.0).abs().lt(1e-6).float().mean())}))
+ctx.close()
