@@ -2,7 +2,8 @@
 set -x
 timeout 600 python bench.py > gpurun_out/final_b32.log 2>&1; echo b32=$?
 timeout 600 python bench.py --batch 1 --steps 30 > gpurun_out/final_b1.log 2>&1; echo b1=$?
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_b32.csv python bench.py --profile-only --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo l32=$?
-timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -k "regex:k_gemm|k_attn|k_gather" --csv --log-file gpurun_out/traffic_b32.csv python bench.py --profile-only --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo t32=$?
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gemm --launch-skip 11 --launch-count 1 -f -o gpurun_out/prof_gemm_gu_b32 python bench.py --profile-only --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo g=$?
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_attn_pair --launch-skip 3 --launch-count 1 -f -o gpurun_out/prof_pair_b32 python bench.py --profile-only --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo a=$?
+# launch list of one cfg3 batch-32 step (our kernels only; ncu serialises launches and runs them cold)
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -k "regex:^k_|k_gemm|k_attn" --csv --log-file gpurun_out/launches_b32.csv python bench.py --profile-only --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo l32=$?
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -k "regex:^k_|k_gemm|k_attn" --csv --log-file gpurun_out/launches_b1.csv python bench.py --profile-only --batch 1 --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo l1=$?
+# one selective-layer gate/up GEMM (CTA pair) at batch 32, full set
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_gemm_pair --launch-skip 7 --launch-count 1 -f -o gpurun_out/prof_gemm_pair_b32 python bench.py --profile-only --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo g=$?
