@@ -340,8 +340,10 @@ def run_reference(args, wl):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators)",
-           "config": {"workload": wl.name, "batch": 1, "seq_len": wl.n, "r": r_bp / 1e4,
-                      "check_layer": args.check_layer},
+           "config": {"workload": wl.name, "batch": args.batch or wl.batch, "seq_len": wl.n, "r": r_bp / 1e4,
+                      "check_layer": args.check_layer, "parallelism": "dp1",
+                      "sample": "each step = one request of the batch (the oracle serves requests one at a time; "
+                                "tok/s is independent of the batch size)"},
            "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
