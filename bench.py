@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines, no oracle)")
+    ap.add_argument("--poisson-qps", type=float, default=0.0,
+                    help="serving mode (SURVEY §8(d) config 4 on one GPU): open-loop Poisson arrivals at this rate, "
+                         "dynamic batching up to --batch; reports TTFT p50/p99 (arrival -> logits on the device)")
+    ap.add_argument("--requests", type=int, default=400, help="requests in the Poisson run")
     ap.add_argument("--host-frac", type=float, default=0.0,
                     help="NEXT-2: this fraction of the catalog lives only in the pinned host tier; each batch's "
                          "host-tier candidates are pulled by rc_fetch_host on a side stream during the previous batch")
@@ -591,6 +595,66 @@ def baselines(args, wl, env, r_bp, c, step_ms):
     return out
 
 
+def run_poisson(args, wl):
+    """Open-loop Poisson arrivals on one GPU: whenever the device is free, every request that has
+    arrived (up to --batch) is assembled and prefilled as one ragged batch; a request's TTFT is the
+    wall-clock time from its arrival to its batch's logits being complete on the device."""
+    import time
+    import torch
+    from paper_2605_07443_b200.build import build
+    device = torch.device("cuda", 0)
+    torch.cuda.set_device(device)
+    build()
+    max_b = args.batch or wl.batch
+    n = args.requests
+    env = build_ours(wl, max_b, (n + max_b - 1) // max_b, 0, device)
+    ctx = env["ctx"]
+    lays = [l for b in env["batches"] for l in b][:n]
+    r_bp, c = args.r_bp or wl.r_bp, args.check_layer
+    stream = torch.cuda.current_stream(device)
+    rng = np.random.default_rng(17)
+    arrivals = np.cumsum(rng.exponential(1.0 / args.poisson_qps, n))
+
+    def serve(batch_lays):
+        seqs = ctx.assemble(batch_lays, prefix_id=1, gather_from=c, stream=stream)
+        ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False,
+                              n_cand=sum(len(l["cand_idtok"]) for l in batch_lays), stream=stream)
+        ctx.release(seqs)
+
+    for k in range(3):  # warm-up at the largest batch
+        serve(lays[:max_b])
+    torch.cuda.synchronize(device)
+    ttft, sizes = np.zeros(n), []
+    i, queue = 0, []
+    t0 = time.perf_counter()
+    done = 0
+    while done < n:
+        now = time.perf_counter() - t0
+        while i < n and arrivals[i] <= now:
+            queue.append(i)
+            i += 1
+        if not queue:
+            time.sleep(max(0.0, arrivals[i] - (time.perf_counter() - t0)))
+            continue
+        batch, queue = queue[:max_b], queue[max_b:]
+        serve([lays[r] for r in batch])
+        torch.cuda.synchronize(device)
+        t_done = time.perf_counter() - t0
+        for r in batch:
+            ttft[r] = (t_done - arrivals[r]) * 1e3
+        sizes.append(len(batch))
+        done += len(batch)
+    span = time.perf_counter() - t0
+    out = {"metric": METRIC, "mode": "poisson", "qps": args.poisson_qps, "requests": n, "max_batch": max_b,
+           "config": {"workload": wl.name, "seq_len": wl.n, "r": r_bp / 1e4, "check_layer": c},
+           "ttft_ms": {"p50": float(np.percentile(ttft, 50, method="inverted_cdf")),
+                       "p99": float(np.percentile(ttft, 99, method="inverted_cdf")), "mean": float(ttft.mean())},
+           "served_tok_s": n * wl.n / span, "batches": len(sizes), "mean_batch": float(np.mean(sizes)),
+           "timing": "wall clock: arrival (seeded exponential gaps) -> device synchronize after the batch's LM head"}
+    print(json.dumps(out))
+    ctx.close()
+
+
 def main():
     args = parse()
     if os.environ.get("RC_WATCHDOG"):
@@ -600,6 +664,8 @@ def main():
     wl = rcgen.WORKLOADS[args.config]
     if args.impl == "reference":
         run_reference(args, wl)
+    elif args.poisson_qps > 0:
+        run_poisson(args, wl)
     else:
         run_ours(args, wl)
 
