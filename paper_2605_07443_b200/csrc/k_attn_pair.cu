@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int nk[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    tl[t] = a.tiles[2 * blockIdx.x + t];
+    tl[t] = a.tiles[2 * (gridDim.x - 1 - blockIdx.x) + t];  // last-first: the longest causal pairs start first
     nk[t] = tl[t].y > 0 ? a.qpos[tl[t].x + tl[t].y - 1] / BKV + 1 : 0;  // rows sorted by position
   }
   const int nkv = max(nk[0], nk[1]);

@@ -74,7 +74,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem = *tmem_slot;
   griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
   griddep_launch();
-  const int4 tile = a.tiles[blockIdx.x];
+  // tiles of a request are in position order and the causal KV grows with position: launch them
+  // last-first, so the longest tiles start in the first wave and short ones fill the tail
+  const int tix = gridDim.x - 1 - blockIdx.x;
+  const int4 tile = a.tiles[tix];
   const int row_start = tile.x, n_rows = tile.y, kv_base = tile.z;
   const int kvh = blockIdx.y;
   const int G = a.n_heads / a.n_kv_heads;
@@ -232,11 +235,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     const bool split = nsp > 1;
     if (a.split_min > 0 && tile.w == 0 && r == 0 && h == 0)
-      a.split_flag[(blockIdx.x / a.n_splits) * a.n_kv_heads + kvh] = split ? 1 : 0;
+      a.split_flag[(tix / a.n_splits) * a.n_kv_heads + kvh] = split ? 1 : 0;
     // this thread writes output columns [h*64, h*64 + 64) of its row: bf16 into o, or (KV split) the
     // fp32 partial normalised by its own l plus (m, l) for the merge kernel
     uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + h * 64;
-    const int64_t prow = (static_cast<int64_t>(blockIdx.x) * a.n_kv_heads + kvh) * ROWS + r;
+    const int64_t prow = (static_cast<int64_t>(tix) * a.n_kv_heads + kvh) * ROWS + r;
     float* pdst = split ? a.part_o + prow * DH + h * 64 : nullptr;
     if (split && h == 0 && !idle) {
       a.part_ml[prow * 2] = m;
