@@ -28,7 +28,7 @@ constexpr uint32_t HALF = ROWS * 64 * 2;  // one [128 rows][64 bf16] SW128 sub-t
 constexpr uint32_t TILE = 2 * HALF;       // 32 KB
 constexpr int SCOLS = 64;                  // keys per softmax thread per tile (two key halves)
 constexpr int NTHREADS = 128 + 256;        // 4 control warps + 2 x 4 softmax warps
-constexpr int KST = 2, VST = 2;
+constexpr int KST = 3, VST = 3;  // 3-deep K and V rings: one-request grids are bound by the K/V load latency
 constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
 constexpr uint32_t OFF_RED = OFF_BAR + 256;  // [2 halves][2 (m, l)][128 rows] f32 for the final merge
 constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
@@ -126,12 +126,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t idPV = idesc_bf16_f32_bmn(128, 128);
       mbar_wait(q_full, 0);
       tc_fence_after();
+      const bool no_mma = (a.debug_mode & 2) != 0;  // diagnostics: barriers only
       auto issue_s = [&](int j) {  // S_j into buffer j % 2
         const int s = j % KST;
         mbar_wait(&k_full[s], (j / KST) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < DH / 16; ++k) {
+        for (int k = 0; k < (no_mma ? 0 : DH / 16); ++k) {
           const uint64_t ad = sdesc_sw128(smem_u32(sQ + (k >> 2) * HALF)) + 2 * (k & 3);
           const uint64_t bd = sdesc_sw128(smem_u32(sK + s * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
           umma_bf16(tmem + (j & 1) * 128, ad, bd, idS, k > 0);
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&p_full[b * 2 + h], (j >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 64 keys: A = P_{j,h} (8 TMEM columns per 16 keys), B = V rows
+          for (int k = 0; k < (no_mma ? 0 : 4); ++k) {  // 64 keys: A = P_{j,h} (8 TMEM columns per 16 keys), B = V rows
             const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + v * TILE + (4 * h + k) * 2048), HALF, 1024);
             umma_bf16_ts(tmem + O_COL + h * 128, tmem + b * 128 + h * 64 + k * 8, bd, idPV,
                          (j > 0 || k > 0) ? 1u : 0u);
@@ -176,6 +177,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
+      if (a.debug_mode & 1) {  // diagnostics: no softmax work
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b * 2 + h]);
+        continue;
+      }
       tmem_ld32(tmem + lane_base + b * 128 + col0, sr);
       tmem_ld32(tmem + lane_base + b * 128 + col0 + 32, sr + 32);
       tmem_wait_ld();
