@@ -36,25 +36,23 @@ _LOGITS = {}
 CHECK_REQS = tuple(int(x) for x in os.environ.get("RC_FULLSIZE_REQS", "0,31").split(","))
 
 
-@pytest.fixture(scope="module")
-def run():
+def _setup(wl, batch, check_reqs):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2605_07443_b200.build import build
     from paper_2605_07443_b200.api import RcContext
     from paper_2605_07443_b200 import _lib as R
     build()
-    wl = rcgen.CFG3
     shape = wl.shape
     dev = torch.device("cuda", 0)
     W = rcgen.gen_weights(shape, seed=0, device=dev)
     cat, protos, sys_tok = rcgen.gen_catalog(wl), rcgen.gen_protos(wl), rcgen.gen_system_prompt(wl)
-    reqs = rcgen.gen_requests(wl, cat, protos, wl.batch, start=0)  # bench.py's first batch at N=1
+    reqs = rcgen.gen_requests(wl, cat, protos, batch, start=0)  # bench.py's first batch at N=1
     items = sorted({int(i) for r in reqs for i in r.cand_items})
     pids = sorted({int(p) for r in reqs for p in r.hist_protos})
     n = wl.n
     ctx = RcContext(shape, W, item_rows=len(items) * wl.item_len, hist_rows=len(pids), prefix_rows=wl.prefix_len,
-                    arena_rows=wl.batch * n, max_seq_len=n, max_batch_tokens=wl.batch * n)
+                    arena_rows=batch * n, max_seq_len=n, max_batch_tokens=batch * n)
     for i0 in range(0, len(items), 128):
         ids = items[i0:i0 + 128]
         kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=dev)
@@ -72,7 +70,7 @@ def run():
     torch.cuda.synchronize()
     res = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
     res["kv_last"] = {r: tuple(t.cpu().numpy().view(np.uint16) for t in ctx.read_kv(seqs[r], shape.n_layers - 1, n))
-                      for r in CHECK_REQS}
+                      for r in check_reqs}
     cand_off = np.concatenate([[0], np.cumsum([len(l["cand_idtok"]) for l in lays])])
     ctx.release(seqs)
     ctx.close()
@@ -84,6 +82,11 @@ def run():
     del W
     torch.cuda.empty_cache()
     return res, ctxd
+
+
+@pytest.fixture(scope="module")
+def run():
+    return _setup(rcgen.CFG3, rcgen.CFG3.batch, CHECK_REQS)
 
 
 def _oracle(d, r, sel):
@@ -140,3 +143,25 @@ def test_cfg3_batch32_logits_over_checked_set():
     got = np.concatenate([_LOGITS[r][0] for r in CHECK_REQS])
     ref = np.concatenate([_LOGITS[r][1] for r in CHECK_REQS])
     assert rel_l2(got, ref) < TOL
+
+
+def test_cfg5_qwen2_8k_batch4_request_matches_oracle():
+    """Config 5 shape at full size: Qwen2-7B (28 layers, GQA 7, QKV bias), 8192-token prompts -- the
+    R6 key packing limit (positions up to 8191) -- in a batch of 4; the last request is checked end
+    to end against the oracle (same bounds as cfg3)."""
+    wl = rcgen.CFG5
+    res, d = _setup(wl, 4, (3,))
+    r = 3
+    L = d["shape"].n_layers
+    off = res["sel_off"]
+    sel = res["sel_pos"][off[r]:off[r + 1]]
+    assert sel[-1] == wl.n - 1 == 8191 and list(sel) == sorted(set(sel.tolist()))
+    lay, K_asm, dfn, forced, own = _oracle(d, r, sel)
+    jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
+    Kg = bf16_to_f32(res["kv_last"][r][0])[sel].astype(np.float64)
+    err = {"jaccard": jac, "logits": rel_l2(res["logits"][r], forced["logits"]),
+           "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
+           "K_last": rel_l2(Kg, forced["K"][L - 1][sel])}
+    print("fullsize cfg5 parity", json.dumps(err))
+    assert jac >= 0.8, err
+    assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
