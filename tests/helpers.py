@@ -77,3 +77,26 @@ def rel_l2(a, b):
     a = np.asarray(a, dtype=np.float64).ravel()
     b = np.asarray(b, dtype=np.float64).ravel()
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def assert_top10_ranking(gpu_scores, ref_scores, logit_err):
+    """R19 / north star "identical top-10 candidate ranking": rank = score desc, ties -> lower slot.
+    logit_err = the measured RMS error of the request's logits (GPU vs oracle). Wherever the
+    oracle's gap between its i-th and (i+1)-th candidate exceeds 4 logit_err, the GPU's top-(i+1)
+    set must equal the oracle's (near-ties may swap). Returns the number of positions checked."""
+    g = np.asarray(gpu_scores, dtype=np.float64)
+    r = np.asarray(ref_scores, dtype=np.float64)
+    order_r = sorted(range(len(r)), key=lambda i: (-r[i], i))
+    order_g = sorted(range(len(g)), key=lambda i: (-g[i], i))
+    checked = 0
+    for i in range(min(10, len(r) - 1)):
+        if r[order_r[i]] - r[order_r[i + 1]] > 4 * logit_err:
+            assert set(order_g[:i + 1]) == set(order_r[:i + 1]), (i, order_g[:11], order_r[:11], logit_err)
+            checked += 1
+    return checked
+
+
+def rms_err(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return float(np.sqrt(np.mean((a - b) ** 2)))

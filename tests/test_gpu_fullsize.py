@@ -24,7 +24,7 @@ from oracle.layout import layout_from_request
 from oracle.model import OracleModel
 from oracle.numerics import bf16_to_f32
 from oracle.selective import selective_prefill
-from tests.helpers import rel_l2
+from tests.helpers import rel_l2, assert_top10_ranking, rms_err
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
@@ -134,6 +134,8 @@ def test_cfg3_batch32_request_matches_oracle(run, r):
     cs = res["cand_scores"][d["cand_off"][r]:d["cand_off"][r + 1]]
     ref = forced["cand_scores"]
     assert np.allclose(cs, ref, rtol=0.05, atol=0.05 * np.abs(ref).max())
+    print("fullsize ranking: resolvable top-10 positions checked",
+          assert_top10_ranking(cs, ref, rms_err(res["logits"][r], forced["logits"])))
 
 
 def test_cfg3_batch32_logits_over_checked_set():

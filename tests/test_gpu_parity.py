@@ -16,7 +16,7 @@ from oracle.model import OracleModel, full_prefill, forward
 from oracle.numerics import bf16_bits, bf16_to_f32, deviation_fixed
 from oracle.select import select_sel
 from oracle.selective import selective_prefill
-from tests.helpers import make_case, oracle_pools, layouts, rel_l2
+from tests.helpers import make_case, oracle_pools, layouts, rel_l2, assert_top10_ranking, rms_err
 
 pytestmark = pytest.mark.gpu
 
@@ -214,6 +214,7 @@ def test_selective_prefill_parity(wl, r_bp, c):
     if len(keep):
         assert np.array_equal(res["kv_last"][0][0][keep], K_asm[L - 1][keep])
     assert np.allclose(res["cand_scores"], forced["cand_scores"], rtol=0.05, atol=0.05 * np.abs(forced["cand_scores"]).max())
+    assert_top10_ranking(res["cand_scores"], forced["cand_scores"], rms_err(res["logits"][0], forced["logits"]))
 
 
 def test_ragged_batch_matches_per_request():

@@ -172,3 +172,14 @@ def test_combine_fixed_reductions_and_rounding():
     # 3.5 -> 4, 2.5 -> 2 (half to even), 4.5 -> 4, 7 -> 7
     assert combine_fixed(A, D, 0.5)[:4].tolist() == [4, 2, 4, 7]
     assert int(combine_fixed(A, D, 0.5)[4]) == (2 ** 40 + 2 ** 50) // 2
+
+
+def test_top10_ranking_helper():
+    from tests.helpers import assert_top10_ranking
+    ref = np.array([5.0, 4.0, 3.9999, 1.0, 0.5, 9.0, 2.0, 2.5, 3.0, 0.1, 0.2, 7.0])
+    assert assert_top10_ranking(ref + 1e-6, ref, 1e-3) >= 8     # all resolvable gaps agree
+    near = ref.copy(); near[1], near[2] = ref[2], ref[1]       # swap inside a near-tie: allowed
+    assert_top10_ranking(near, ref, 1e-3)
+    bad = ref.copy(); bad[5], bad[11] = ref[11], ref[5]        # a candidate far off its logit error: caught
+    with pytest.raises(AssertionError):
+        assert_top10_ranking(bad, ref, 1e-3)
