@@ -28,7 +28,11 @@ constexpr uint32_t HALF = ROWS * 64 * 2;  // one [128 rows][64 bf16] SW128 sub-t
 constexpr uint32_t TILE = 2 * HALF;       // 32 KB
 constexpr int SCOLS = 64;                  // keys per softmax thread per tile (two key halves)
 constexpr int NTHREADS = 128 + 256;        // 4 control warps + 2 x 4 softmax warps
-constexpr int KST = 3, VST = 3;  // 3-deep K and V rings: one-request grids are bound by the K/V load latency
+// 2-deep K and V rings whose "empty" events are the MMA commits that already exist: K_j's slot is
+// free once S_j is complete (s_full[j & 1]) and V_j's once both PV halves of step j are
+// (pv_done[j & 1]), so the single MMA thread commits twice per KV step instead of five times
+// (its serial barrier work bounds a one-request grid)
+constexpr int KST = 2, VST = 2;
 constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
 constexpr uint32_t OFF_RED = OFF_BAR + 256;  // [2 halves][2 (m, l)][128 rows] f32 for the final merge
 constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
@@ -49,21 +53,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* q_full = bars;                 // [1]
   uint64_t* k_full = bars + 1;             // [KST]
-  uint64_t* k_empty = k_full + KST;        // [KST]
-  uint64_t* v_full = k_empty + KST;        // [VST]
-  uint64_t* v_empty = v_full + VST;        // [VST]
-  uint64_t* s_full = v_empty + VST;        // [2]
+  uint64_t* v_full = k_full + KST;         // [VST]
+  uint64_t* s_full = v_full + VST;         // [2]  S_j complete (also: K slot j & 1 free)
   uint64_t* p_full = s_full + 2;           // [2 S buffers][2 halves]
-  uint64_t* pv_done = p_full + 4;          // [2 halves][2] alternating per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 4);
+  uint64_t* pv_done = p_full + 4;          // [2]  both PV halves of step j complete (also: V slot free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
-    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 4; ++i) { mbar_init(&p_full[i], 4); mbar_init(&pv_done[i], 1); }  // p_full: 1 per warp
+    for (int i = 0; i < KST; ++i) mbar_init(&k_full[i], 1);
+    for (int i = 0; i < VST; ++i) mbar_init(&v_full[i], 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&pv_done[i], 1); }
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // p_full: 1 per warp
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int krow0 = static_cast<int>(kvh * t_cap + kv_base) + j0 * BKV;
       for (int j = 0; j < nkv; ++j) {
         const int s = j % KST;
-        mbar_wait(&k_empty[s], ((j / KST) & 1) ^ 1);
+        mbar_wait(&s_full[s], ((j / KST) & 1) ^ 1);  // S_{j-2} complete: slot s is free
         mbar_expect_tx(&k_full[s], TILE);
         tma_load_2d(sK + s * TILE, &tmK, &k_full[s], 0, krow0 + j * BKV);
         tma_load_2d(sK + s * TILE + HALF, &tmK, &k_full[s], 64, krow0 + j * BKV);
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int vrow0 = static_cast<int>(kvh * t_cap + kv_base) + j0 * BKV;
       for (int j = 0; j < nkv; ++j) {
         const int s = j % VST;
-        mbar_wait(&v_empty[s], ((j / VST) & 1) ^ 1);
+        mbar_wait(&pv_done[s], ((j / VST) & 1) ^ 1);  // PV_{j-2} complete: slot s is free
         mbar_expect_tx(&v_full[s], TILE);
         tma_load_2d(sV + s * TILE, &tmV, &v_full[s], 0, vrow0 + j * BKV);
         tma_load_2d(sV + s * TILE + HALF, &tmV, &v_full[s], 64, vrow0 + j * BKV);
@@ -137,7 +139,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint64_t bd = sdesc_sw128(smem_u32(sK + s * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
           umma_bf16(tmem + (j & 1) * 128, ad, bd, idS, k > 0);
         }
-        umma_commit(&k_empty[s]);
         umma_commit(&s_full[j & 1]);
       };
       if (nkv > 0) issue_s(0);
@@ -154,9 +155,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             umma_bf16_ts(tmem + O_COL + h * 128, tmem + b * 128 + h * 64 + k * 8, bd, idPV,
                          (j > 0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&pv_done[h * 2 + (j & 1)]);
         }
-        umma_commit(&v_empty[v]);
+        umma_commit(&pv_done[j & 1]);
         if (j + 2 < nkv) issue_s(j + 2);  // buffer b: both halves' P_j consumed by the PVs just issued
       }
     }
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         m_run = m_new;
       }
       if (j > 0 && __any_sync(0xffffffffu, need)) {  // rescale this group's accumulator rows (rare)
-        mbar_wait(&pv_done[h * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+        mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         tc_fence_after();
         uint32_t o[32];
 #pragma unroll
@@ -235,8 +235,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
     const float w0 = f0 * inv, w1 = f1 * inv;
     if (nkv > 0) {
-      mbar_wait(&pv_done[0 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
-      mbar_wait(&pv_done[1 * 2 + ((nkv - 1) & 1)], ((nkv - 1) >> 1) & 1);
+      mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     }
     tc_fence_after();
     const bool split = nsp > 1;
