@@ -380,7 +380,9 @@ __device__ __forceinline__ float sm_exp_pack64(const uint32_t* sr, uint32_t* pk,
     }
     const int chunk = c >> 3;
     if (chunk == 2 || chunk == 5 || chunk == 7) {
-      const uint64_t xc = f2_pack(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+      // clamp to [-127, 65]: no exponent wrap; a speculative base more than 64 below the row max
+      // still shows up as P >= 2^65 in the row sum
+      const uint64_t xc = f2_pack(fminf(fmaxf(x0, -127.f), 65.f), fminf(fmaxf(x1, -127.f), 65.f));
       const uint64_t t2 = f2_add(xc, mg2);
       const uint64_t f = f2_sub(xc, f2_sub(t2, mg2));
       uint64_t pp = f2_fma(f, c3, c2);

@@ -35,6 +35,7 @@ constexpr uint32_t OFF_Q = 0, OFF_K = 2 * TILE, OFF_V = OFF_K + KST * TILE, OFF_
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
 constexpr uint32_t O_COL = 256;            // O_t at 256 + 128 t
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
+constexpr float SPEC_SUM_MAX = 18446744073709551616.0f;  // 2^64: bound of the speculative exps' row sum
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -185,7 +186,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int p_first = n_t > 0 ? a.qpos[row_start] : 0;  // smallest position of the tile
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t s_col = tmem + lane_base + t * 128;
-    float m_run = -INFINITY, l_run = 0.f;
+    // padding rows see no key: base 0 keeps them off the max-first path (their P is 0, l stays 0)
+    float m_run = valid ? -INFINITY : 0.f, l_run = 0.f;
     for (int j = 0; j < n_t; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
@@ -202,6 +204,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_wait_ld();
         const int key0 = j * BKV + hh * 64;
         const bool full = key0 + 63 <= p_first;  // every row sees every key of the half: no causal mask
+        uint32_t pk[32];
+        // common case: exps against the running max, no row-max pass at all. Kept unless some row's sum
+        // exceeds 2^64 (then some P > 2^64, or inf/NaN): the half is redone below with the max first.
+        // Any P <= 2^64 keeps O and l finite over 8192 keys, and bf16/fp32 precision is relative.
+        if ((a.debug_mode & 4) == 0 && !__any_sync(0xffffffffu, m_run == -INFINITY)) {
+          const float ls = full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, m_run)
+                                : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, m_run);
+          if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
+            l_run += ls;
+            tmem_st32(s_col + hh * 32, pk);
+            continue;
+          }
+        }
         const float rmax = full ? sm_rowmax64<false>(sr, key0, p) : sm_rowmax64<true>(sr, key0, p);
         // raw scores; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
         const float mx = rmax * a.scale_log2;
@@ -238,7 +253,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         l_run *= alpha;
         const float base = (m_run == -INFINITY) ? 0.f : m_run;
-        uint32_t pk[32];
         l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
                       : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
         tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)

@@ -38,6 +38,7 @@ constexpr uint32_t OFF_RED = OFF_BAR + 256;  // [2 halves][2 (m, l)][128 rows] f
 constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
 constexpr uint32_t O_COL = 256;            // O_h at 256 + 128 h
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
+constexpr float SPEC_SUM_MAX = 18446744073709551616.0f;  // 2^64: bound of the speculative exps' row sum
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int p_first = a.qpos[row_start];  // smallest position of the tile (rows sorted by position)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t o_col = O_COL + h * 128;
-    float m_run = -INFINITY, l_run = 0.f;
+    // padding rows see no key: base 0 keeps them off the max-first path (their P is 0, l stays 0)
+    float m_run = valid ? -INFINITY : 0.f, l_run = 0.f;
     uint32_t sr[SCOLS];
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
@@ -187,6 +189,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_wait_ld();
       const int key0 = (j0 + j) * BKV + col0;
       const bool full = key0 + SCOLS - 1 <= p_first;  // every row sees every key of the half: no mask
+      uint32_t pk[SCOLS / 2];
+      // common case: exps against the running max, no row-max pass at all. Kept unless some row's sum
+      // exceeds 2^64 (then some P > 2^64, or inf/NaN): the step is redone below with the max first.
+      // Any P <= 2^64 keeps O and l finite over 8192 keys, and bf16/fp32 precision is relative.
+      if ((a.debug_mode & 4) == 0 && !__any_sync(0xffffffffu, m_run == -INFINITY)) {
+        const float ls = full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, m_run)
+                              : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, m_run);
+        if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
+          l_run += ls;
+          tmem_st32(tmem + lane_base + b * 128 + col0, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[b * 2 + h]);
+          continue;
+        }
+      }
       // scores stay raw; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
       const float mx = (full ? sm_rowmax64<false>(sr, key0, p) : sm_rowmax64<true>(sr, key0, p)) * a.scale_log2;
       float alpha = 1.f;
@@ -213,7 +232,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       l_run *= alpha;
       const float base = (m_run == -INFINITY) ? 0.f : m_run;
       // P (bf16 pairs) overwrites the first 32 of this group's own 64 S columns (already in registers)
-      uint32_t pk[SCOLS / 2];
       l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
                     : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
       tmem_st32(tmem + lane_base + b * 128 + col0, pk);
