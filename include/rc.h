@@ -49,7 +49,7 @@ enum { RC_POOL_ITEM_BF16 = 0, RC_POOL_HIST_INT8 = 1, RC_POOL_PREFIX_BF16 = 2, RC
 enum { RC_TOK_PREFIX = 0, RC_TOK_FORCED = 1, RC_TOK_HIST = 2, RC_TOK_ITEM = 3 };
 enum { RC_MISS_ERROR = 0, RC_MISS_RECOMPUTE = 1 };
 
-/* Decoder shape (Llama / Qwen2 family). head_dim in {16, 64, 128}. */
+/* Decoder shape (Llama / Qwen2 family). head_dim in {16, 64, 128}; d_model <= 8192. */
 typedef struct rc_model_desc {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
   double rope_theta; /* RoPE base (rotate-half pairs) */

@@ -34,6 +34,9 @@ __global__ void k_embed(const uint16_t* __restrict__ emb, const int32_t* __restr
   }
 }
 
+// One CTA per row; the row stays in registers between the sum of squares and the scaled write
+// (V float4 per thread, one load round trip). Same summation order as a strided loop.
+template <int V>
 __global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, const int32_t* __restrict__ row_idx,
                                                  int32_t d, const uint16_t* __restrict__ g, float eps,
                                                  uint16_t* __restrict__ out) {
@@ -43,11 +46,19 @@ __global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, co
   const int r = blockIdx.x;
   const int64_t src = row_idx ? row_idx[r] : r;
   const float4* xr = reinterpret_cast<const float4*>(x + src * d);
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
-    const float4 v = xr[i];
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  const uint2* grow = reinterpret_cast<const uint2*>(g);
+  const int n4 = d / 4;
+  float4 v[V];
+  uint2 gg[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    gg[k] = i < n4 ? __ldg(&grow[i]) : make_uint2(0u, 0u);
   }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
 #pragma unroll
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
@@ -61,13 +72,13 @@ __global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, co
   __syncthreads();
   const float inv = rsqrtf(red[0] / d + eps);
   uint2* orow = reinterpret_cast<uint2*>(out + static_cast<int64_t>(r) * d);
-  const uint2* grow = reinterpret_cast<const uint2*>(g);
-  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
-    const float4 v = xr[i];
-    const uint2 gg = __ldg(&grow[i]);
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i >= n4) break;
     uint2 o;
-    o.x = pack_bf2(v.x * inv * __uint_as_float(gg.x << 16), v.y * inv * __uint_as_float(gg.x & 0xFFFF0000u));
-    o.y = pack_bf2(v.z * inv * __uint_as_float(gg.y << 16), v.w * inv * __uint_as_float(gg.y & 0xFFFF0000u));
+    o.x = pack_bf2(v[k].x * inv * __uint_as_float(gg[k].x << 16), v[k].y * inv * __uint_as_float(gg[k].x & 0xFFFF0000u));
+    o.y = pack_bf2(v[k].z * inv * __uint_as_float(gg[k].y << 16), v[k].w * inv * __uint_as_float(gg[k].y & 0xFFFF0000u));
     orow[i] = o;
   }
 }
@@ -292,7 +303,12 @@ cudaError_t rmsnorm_launch(const float* x, const int32_t* row_idx, int32_t rows,
                            uint16_t* out, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
   const int th = d >= 1024 ? 256 : 64;
-  return launch_pdl(k_rmsnorm, dim3(rows), dim3(th), 0, s, x, row_idx, d, g, eps, out);
+  const int per = (d / 4 + th - 1) / th;  // float4 per thread
+  if (per <= 1) return launch_pdl(k_rmsnorm<1>, dim3(rows), dim3(th), 0, s, x, row_idx, d, g, eps, out);
+  if (per <= 2) return launch_pdl(k_rmsnorm<2>, dim3(rows), dim3(th), 0, s, x, row_idx, d, g, eps, out);
+  if (per <= 4) return launch_pdl(k_rmsnorm<4>, dim3(rows), dim3(th), 0, s, x, row_idx, d, g, eps, out);
+  if (per <= 8) return launch_pdl(k_rmsnorm<8>, dim3(rows), dim3(th), 0, s, x, row_idx, d, g, eps, out);
+  return cudaErrorInvalidValue;  // d > 8192: not a supported model width
 }
 cudaError_t gather_rows_f32_launch(const float* src, const int32_t* idx, int32_t rows, int32_t d, float* dst,
                                    cudaStream_t s) {

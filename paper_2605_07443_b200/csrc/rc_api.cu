@@ -337,7 +337,7 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   const rc_model_desc& m = *md;
   if (m.n_layers <= 0 || m.d_model <= 0 || m.n_heads <= 0 || m.n_kv_heads <= 0 || m.n_heads % m.n_kv_heads ||
       !(m.head_dim == 16 || m.head_dim == 64 || m.head_dim == 128) || m.d_ff % 128 || m.d_model % 64 != 0 &&
-      m.d_model % 16 != 0)
+      m.d_model % 16 != 0 || m.d_model > 8192)
     return fail(RC_E_INVALID, "unsupported model shape");
   if (pd->max_seq_len <= 0 || pd->max_seq_len > 8192) return fail(RC_E_INVALID, "max_seq_len must be in 1..8192 (R6)");
   if (pd->max_batch_tokens <= 0 || pd->remote_rows > pd->item_rows) return fail(RC_E_INVALID, "bad pool desc");
