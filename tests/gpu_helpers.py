@@ -14,7 +14,7 @@ def weights_to(W, device="cuda"):
             "layers": [{k: v.to(device).contiguous() for k, v in lw.items()} for lw in W["layers"]]}
 
 
-def make_ctx(case, pools, n_req_tokens, arena_rows=None, remote_rows=0, Wd=None, extra_item_rows=0):
+def make_ctx(case, pools, n_req_tokens, arena_rows=None, remote_rows=0, Wd=None, extra_item_rows=0, items=None):
     wl, shape = case["wl"], case["shape"]
     Wd = Wd if Wd is not None else weights_to(case["W"])
     n_items = len(pools["item_ids"])
@@ -22,7 +22,7 @@ def make_ctx(case, pools, n_req_tokens, arena_rows=None, remote_rows=0, Wd=None,
                     hist_rows=max(len(pools["proto_ids"]), 1), prefix_rows=max(wl.prefix_len, 1),
                     arena_rows=arena_rows or n_req_tokens, max_seq_len=max(wl.n, 256),
                     max_batch_tokens=n_req_tokens, remote_rows=remote_rows)
-    register_pools(ctx, case, pools)
+    register_pools(ctx, case, pools, items=items)
     return ctx, Wd
 
 
