@@ -3,10 +3,12 @@
 // (batch 32: thousands of tiles), where the single-tile kernel (k_attn_tc.cu) is bound by the L2->SM
 // stream of K/V tiles: every K/V tile is fetched once per 128 query rows.
 //
-// CTA = (two query tiles of ONE request, kv head): Q_0, Q_1 stay in shared memory and every K/V tile
-// is loaded once for both, halving the K/V bytes per FLOP. Tile t <-> TMEM S_t (columns 128 t) and
-// O_t (columns 256 + 128 t); row r of a tile <-> TMEM lane r.
-//   warp 0 lane 0   TMA: Q_0, Q_1 once (3-D boxes [TQ][G][64] x 2 halves), K tiles (2-stage ring)
+// Work item = (two query tiles of ONE request, kv head): Q_0, Q_1 stay in shared memory and every
+// K/V tile is loaded once for both, halving the K/V bytes per FLOP. Persistent CTAs (one per SM)
+// take items from a global counter. Tile t <-> TMEM S_t (columns 128 t) and O_t (columns 256 + 128 t);
+// row r of a tile <-> TMEM lane r.
+//   warp 0 lane 0   scheduler (publishes each item to the other roles) + TMA: Q_0, Q_1 per item (3-D
+//                   boxes [TQ][G][64] x 2 halves), K tiles (2-stage ring running across items)
 //   warp 3 lane 0   TMA: V tiles (2-stage ring)
 //   warp 1 lane 0   MMA, ping-pong over the two tiles: after softmax t has turned S_t(j) into P_t(j)
 //                   it issues O_t += P_t(j) V_j (TS mode, A = P from TMEM) and immediately
@@ -18,7 +20,7 @@
 //                   whole tile is visible, lazy rescale when the running max grows by > 2^8, P in
 //                   bf16 pairs written back over the S columns already consumed). If the second
 //                   half raises the running max, the first half's stored P is rescaled in TMEM (rare).
-// Tiles: a.tiles holds 2 consecutive entries per CTA, both of the same request (the host pads a
+// Tiles: a.tiles holds 2 consecutive entries per work item, both of the same request (the host pads a
 // request's odd tile count with an empty tile {row, 0, kv_base, 0}).
 #include "common.cuh"
 #include "rc_internal.h"
@@ -32,11 +34,20 @@ constexpr uint32_t TILE = 2 * HALF;       // 32 KB
 constexpr int NTHREADS = 128 + 256;       // 4 control warps + 2 x 4 softmax warps
 constexpr int KST = 2, VST = 2;
 constexpr uint32_t OFF_Q = 0, OFF_K = 2 * TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
+constexpr uint32_t OFF_ITEM = OFF_BAR + 256;  // [2] work-item slots (scheduler -> roles)
+constexpr uint32_t SMEM_BYTES = OFF_ITEM + 16;
 constexpr uint32_t O_COL = 256;            // O_t at 256 + 128 t
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 constexpr float SPEC_SUM_MAX = 18446744073709551616.0f;  // 2^64: bound of the speculative exps' row sum
+constexpr int N_ITEM_CONSUMERS = 2 + 8;    // MMA thread, V producer, 8 softmax warps
 
+// Persistent: grid <= #SMs, each CTA takes work items (tile pair, kv head) from a global counter,
+// longest pairs first, so the next item's Q/K/V loads and first S MMAs overlap the previous item's
+// last softmax steps and output epilogue (a fresh CTA per item re-paid the barrier/TMEM setup and the
+// Q load latency with the tensor pipe idle). Warp 0 lane 0 fetches the item and publishes it in a
+// 2-slot ring (it_full / it_empty); all role loops then follow the same item sequence, and every
+// barrier phase is tracked by counters that run across items. O_t is reused across items: the
+// first PV of tile t in an item waits until the previous item's epilogue has read O_t (o_free).
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_attn_pair(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a, int64_t t_cap) {
@@ -47,22 +58,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* sV = smem + OFF_V;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* q_full = bars;           // [1]
-  uint64_t* k_full = bars + 1;       // [KST]
+  uint64_t* q_empty = q_full + 1;    // [1] every MMA of the item reading Q complete
+  uint64_t* k_full = q_empty + 1;    // [KST]
   uint64_t* k_empty = k_full + KST;  // [KST]
   uint64_t* v_full = k_empty + KST;  // [VST]
   uint64_t* v_empty = v_full + VST;  // [VST]
   uint64_t* s_full = v_empty + VST;  // [2 tiles]
   uint64_t* p_full = s_full + 2;     // [2 tiles]
   uint64_t* o_done = p_full + 2;     // [2 tiles] last PV of the tile complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+  uint64_t* o_free = o_done + 2;     // [2 tiles] epilogue has read O_t
+  uint64_t* it_full = o_free + 2;    // [2] item slot written
+  uint64_t* it_empty = it_full + 2;  // [2] item slot read by every role
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(it_empty + 2);
+  volatile int32_t* item_slot = reinterpret_cast<volatile int32_t*>(smem + OFF_ITEM);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-    // p_full: one arrival per softmax warp (lane 0 after __syncwarp), not per thread
-    for (int t = 0; t < 2; ++t) { mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 4); mbar_init(&o_done[t], 1); }
+    // p_full / o_free: one arrival per softmax warp of the tile (lane 0 after __syncwarp)
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 4); mbar_init(&o_done[t], 1); mbar_init(&o_free[t], 4);
+    }
+    for (int i = 0; i < 2; ++i) { mbar_init(&it_full[i], 1); mbar_init(&it_empty[i], N_ITEM_CONSUMERS); }
     fence_barrier_init();
     fence_proxy_async();
   }
@@ -74,64 +94,100 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   griddep_wait();  // PDL: the prologue above overlapped the previous kernel's tail
   griddep_launch();
 
-  const int kvh = blockIdx.y;
   const int G = a.n_heads / a.n_kv_heads;
   const int TQ = ROWS / G;
   const int H = a.n_heads;
-  int4 tl[2];
-  int nk[2];
+  const int n_pairs = a.n_tiles / 2;
+  const int n_items = n_pairs * a.n_kv_heads;
+  // item w: kv head w % Hk of pair n_pairs - 1 - w / Hk (a request's pairs are in position order, so
+  // the longest causal pairs come first)
+  struct Item { int4 tl[2]; int nk[2]; int nkv, kv_base, kvh; };
+  auto decode = [&](int w) {
+    Item it;
+    const int pr = n_pairs - 1 - w / a.n_kv_heads;
+    it.kvh = w % a.n_kv_heads;
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    tl[t] = a.tiles[2 * (gridDim.x - 1 - blockIdx.x) + t];  // last-first: the longest causal pairs start first
-    nk[t] = tl[t].y > 0 ? a.qpos[tl[t].x + tl[t].y - 1] / BKV + 1 : 0;  // rows sorted by position
-  }
-  const int nkv = max(nk[0], nk[1]);
-  const int kv_base = tl[0].z;
+    for (int t = 0; t < 2; ++t) {
+      it.tl[t] = a.tiles[2 * pr + t];
+      it.nk[t] = it.tl[t].y > 0 ? a.qpos[it.tl[t].x + it.tl[t].y - 1] / BKV + 1 : 0;  // rows sorted by position
+    }
+    it.nkv = max(it.nk[0], it.nk[1]);
+    it.kv_base = it.tl[0].z;
+    return it;
+  };
+  // consumers: item i of this CTA (-1 = no more work); the slot is released right after the read
+  auto next_item = [&](int i, bool warp_wide) {
+    mbar_wait(&it_full[i & 1], (i >> 1) & 1);
+    const int w = item_slot[i & 1];
+    if (warp_wide) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&it_empty[i & 1]);
+    } else {
+      mbar_arrive(&it_empty[i & 1]);
+    }
+    return w;
+  };
 
   if (warp == 0) {
-    if (lane == 0 && nkv > 0) {  // ---- Q + K producer
+    if (lane == 0) {  // ---- scheduler + Q/K producer
       tma_prefetch_desc(&tmQ); tma_prefetch_desc(&tmK);
-      mbar_expect_tx(q_full, ((nk[0] > 0 ? 1u : 0u) + (nk[1] > 0 ? 1u : 0u)) * 2u * 128u * G * TQ);
+      int kc = 0;  // K tiles loaded so far (ring position / phase)
+      for (int i = 0;; ++i) {
+        if (i >= 2) mbar_wait(&it_empty[i & 1], ((i - 2) >> 1) & 1);
+        int w = atomicAdd(a.work_ctr, 1);
+        if (w >= n_items) w = -1;
+        item_slot[i & 1] = w;
+        mbar_arrive(&it_full[i & 1]);  // release: the slot write is visible to the waiters
+        if (w < 0) break;
+        const Item it = decode(w);
+        if (i >= 1) mbar_wait(q_empty, (i - 1) & 1);  // the previous item's S MMAs have read Q
+        mbar_expect_tx(q_full, ((it.nk[0] > 0 ? 1u : 0u) + (it.nk[1] > 0 ? 1u : 0u)) * 2u * 128u * G * TQ);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (nk[t] == 0) continue;
-        tma_load_3d(sQ + t * TILE, &tmQ, q_full, 0, kvh * G, tl[t].x);
-        tma_load_3d(sQ + t * TILE + HALF, &tmQ, q_full, 64, kvh * G, tl[t].x);
-      }
-      const int krow0 = static_cast<int>(kvh * t_cap + kv_base);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % KST;
-        mbar_wait(&k_empty[s], ((j / KST) & 1) ^ 1);
-        mbar_expect_tx(&k_full[s], TILE);
-        tma_load_2d(sK + s * TILE, &tmK, &k_full[s], 0, krow0 + j * BKV);
-        tma_load_2d(sK + s * TILE + HALF, &tmK, &k_full[s], 64, krow0 + j * BKV);
+        for (int t = 0; t < 2; ++t) {
+          if (it.nk[t] == 0) continue;
+          tma_load_3d(sQ + t * TILE, &tmQ, q_full, 0, it.kvh * G, it.tl[t].x);
+          tma_load_3d(sQ + t * TILE + HALF, &tmQ, q_full, 64, it.kvh * G, it.tl[t].x);
+        }
+        const int krow0 = static_cast<int>(it.kvh * t_cap + it.kv_base);
+        for (int j = 0; j < it.nkv; ++j, ++kc) {
+          const int s = kc % KST;
+          mbar_wait(&k_empty[s], ((kc / KST) & 1) ^ 1);
+          mbar_expect_tx(&k_full[s], TILE);
+          tma_load_2d(sK + s * TILE, &tmK, &k_full[s], 0, krow0 + j * BKV);
+          tma_load_2d(sK + s * TILE + HALF, &tmK, &k_full[s], 64, krow0 + j * BKV);
+        }
       }
     }
   } else if (warp == 3) {
-    if (lane == 0 && nkv > 0) {  // ---- V producer
+    if (lane == 0) {  // ---- V producer
       tma_prefetch_desc(&tmV);
-      const int vrow0 = static_cast<int>(kvh * t_cap + kv_base);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % VST;
-        mbar_wait(&v_empty[s], ((j / VST) & 1) ^ 1);
-        mbar_expect_tx(&v_full[s], TILE);
-        tma_load_2d(sV + s * TILE, &tmV, &v_full[s], 0, vrow0 + j * BKV);
-        tma_load_2d(sV + s * TILE + HALF, &tmV, &v_full[s], 64, vrow0 + j * BKV);
+      int vc = 0;
+      for (int i = 0;; ++i) {
+        const int w = next_item(i, false);
+        if (w < 0) break;
+        const Item it = decode(w);
+        const int vrow0 = static_cast<int>(it.kvh * t_cap + it.kv_base);
+        for (int j = 0; j < it.nkv; ++j, ++vc) {
+          const int s = vc % VST;
+          mbar_wait(&v_empty[s], ((vc / VST) & 1) ^ 1);
+          mbar_expect_tx(&v_full[s], TILE);
+          tma_load_2d(sV + s * TILE, &tmV, &v_full[s], 0, vrow0 + j * BKV);
+          tma_load_2d(sV + s * TILE + HALF, &tmV, &v_full[s], 64, vrow0 + j * BKV);
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nkv > 0) {  // ---- MMA issuer
+    if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idS = idesc_bf16_f32(128, 128);
       constexpr uint32_t idPV = idesc_bf16_f32_bmn(128, 128);
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      auto wait_k = [&](int j) {
-        mbar_wait(&k_full[j % KST], (j / KST) & 1);
+      const bool no_mma = (a.debug_mode & 2) != 0;  // diagnostics: barriers only
+      int kc = 0, vc = 0, pc[2] = {0, 0}, n_done[2] = {0, 0};
+      auto wait_k = [&](int g) {
+        mbar_wait(&k_full[g % KST], (g / KST) & 1);
         tc_fence_after();
       };
-      const bool no_mma = (a.debug_mode & 2) != 0;  // diagnostics: barriers only
-      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-        const int s = j % KST;
+      auto issue_s = [&](int t, int g) {  // S_t = Q_t K_g^T (g = global K tile index)
+        const int s = g % KST;
 #pragma unroll
         for (int k = 0; k < (no_mma ? 0 : DH / 16); ++k) {
           const uint64_t ad = sdesc_sw128(smem_u32(sQ + t * TILE + (k >> 2) * HALF)) + 2 * (k & 3);
@@ -140,147 +196,172 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         umma_commit(&s_full[t]);
       };
-      wait_k(0);
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-        if (nk[t] > 0) issue_s(t, 0);
-      umma_commit(&k_empty[0]);
-      for (int j = 0; j < nkv; ++j) {
-        const int v = j % VST;
-        mbar_wait(&v_full[v], (j / VST) & 1);
+      for (int i = 0;; ++i) {
+        const int w = next_item(i, false);
+        if (w < 0) break;
+        const Item it = decode(w);
+        mbar_wait(q_full, i & 1);
         tc_fence_after();
-        bool k_ready = false;
+        wait_k(kc);
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (j >= nk[t]) continue;
-          mbar_wait(&p_full[t], j & 1);
+        for (int t = 0; t < 2; ++t)
+          if (it.nk[t] > 0) issue_s(t, kc);
+        umma_commit(&k_empty[kc % KST]);
+        for (int j = 0; j < it.nkv; ++j) {
+          const int v = (vc + j) % VST;
+          mbar_wait(&v_full[v], ((vc + j) / VST) & 1);
           tc_fence_after();
+          bool k_ready = false;
 #pragma unroll
-          for (int k = 0; k < (no_mma ? 0 : BKV / 16); ++k) {  // 16 keys per MMA: A = P_t (8 TMEM columns), B = V rows
-            const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + v * TILE + k * 2048), HALF, 1024);
-            umma_bf16_ts(tmem + O_COL + t * 128, tmem + t * 128 + k * 8, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
+          for (int t = 0; t < 2; ++t) {
+            if (j >= it.nk[t]) continue;
+            if (j == 0 && n_done[t] > 0) mbar_wait(&o_free[t], (n_done[t] - 1) & 1);  // O_t read out
+            mbar_wait(&p_full[t], pc[t] & 1);
+            ++pc[t];
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < (no_mma ? 0 : BKV / 16); ++k) {  // 16 keys per MMA: A = P_t (8 TMEM columns), B = V rows
+              const uint64_t bd = sdesc_sw128_mn(smem_u32(sV + v * TILE + k * 2048), HALF, 1024);
+              umma_bf16_ts(tmem + O_COL + t * 128, tmem + t * 128 + k * 8, bd, idPV, (j > 0 || k > 0) ? 1u : 0u);
+            }
+            if (j + 1 == it.nk[t]) umma_commit(&o_done[t]);
+            if (j + 1 < it.nk[t]) {
+              if (!k_ready) { wait_k(kc + j + 1); k_ready = true; }
+              issue_s(t, kc + j + 1);
+            }
           }
-          if (j + 1 == nk[t]) umma_commit(&o_done[t]);
-          if (j + 1 < nk[t]) {
-            if (!k_ready) { wait_k(j + 1); k_ready = true; }
-            issue_s(t, j + 1);
+          umma_commit(&v_empty[v]);
+          if (j + 1 < it.nkv) {
+            if (!k_ready) wait_k(kc + j + 1);  // a K tile only the other (finished) tile would have used
+            umma_commit(&k_empty[(kc + j + 1) % KST]);
           }
         }
-        umma_commit(&v_empty[v]);
-        if (j + 1 < nkv) {
-          if (!k_ready) wait_k(j + 1);  // a K tile only the other (finished) tile would have used
-          umma_commit(&k_empty[(j + 1) % KST]);
-        }
+        umma_commit(q_empty);
+        kc += it.nkv;
+        vc += it.nkv;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) n_done[t] += it.nk[t] > 0 ? 1 : 0;
       }
     }
   } else if (warp >= 4) {  // ---- softmax: tile t, thread <-> row
     const int t = (warp - 4) >> 2;
     const int q = warp & 3;  // TMEM lane quarter of this warp
     const int r = q * 32 + lane;
-    const int n_t = t ? nk[1] : nk[0];
-    const int row_start = t ? tl[1].x : tl[0].x;
-    const int n_rows = t ? tl[1].y : tl[0].y;
     const int tt = r / G, g = r % G;
-    const bool valid = (r < TQ * G) && (tt < n_rows);
-    const int p = valid ? a.qpos[row_start + tt] : -1;
-    const int p_first = n_t > 0 ? a.qpos[row_start] : 0;  // smallest position of the tile
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t s_col = tmem + lane_base + t * 128;
-    // padding rows see no key: base 0 keeps them off the max-first path (their P is 0, l stays 0)
-    float m_run = valid ? -INFINITY : 0.f, l_run = 0.f;
-    for (int j = 0; j < n_t; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      if (a.debug_mode & 1) {  // diagnostics: no softmax work
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[t]);
-        continue;
-      }
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t sr[64];
-        tmem_ld32(s_col + hh * 64, sr);
-        tmem_ld32(s_col + hh * 64 + 32, sr + 32);
-        tmem_wait_ld();
-        const int key0 = j * BKV + hh * 64;
-        const bool full = key0 + 63 <= p_first;  // every row sees every key of the half: no causal mask
-        uint32_t pk[32];
-        // common case: exps against the running max, no row-max pass at all. Kept unless some row's sum
-        // exceeds 2^64 (then some P > 2^64, or inf/NaN): the half is redone below with the max first.
-        // Any P <= 2^64 keeps O and l finite over 8192 keys, and bf16/fp32 precision is relative.
-        if ((a.debug_mode & 4) == 0 && !__any_sync(0xffffffffu, m_run == -INFINITY)) {
-          const float ls = full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, m_run)
-                                : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, m_run);
-          if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
-            l_run += ls;
-            tmem_st32(s_col + hh * 32, pk);
-            continue;
-          }
+    int sc = 0, od = 0;  // S_t commits consumed, items with tile t non-empty
+    for (int i = 0;; ++i) {
+      const int w = next_item(i, true);
+      if (w < 0) break;
+      const Item it = decode(w);
+      const int n_t = it.nk[t];
+      if (n_t == 0) continue;
+      const int row_start = it.tl[t].x;
+      const int n_rows = it.tl[t].y;
+      const bool valid = (r < TQ * G) && (tt < n_rows);
+      const int p = valid ? a.qpos[row_start + tt] : -1;
+      const int p_first = a.qpos[row_start];  // smallest position of the tile
+      // padding rows see no key: base 0 keeps them off the max-first path (their P is 0, l stays 0)
+      float m_run = valid ? -INFINITY : 0.f, l_run = 0.f;
+      for (int j = 0; j < n_t; ++j, ++sc) {
+        mbar_wait(&s_full[t], sc & 1);
+        tc_fence_after();
+        if (a.debug_mode & 1) {  // diagnostics: no softmax work
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[t]);
+          continue;
         }
-        const float rmax = full ? sm_rowmax64<false>(sr, key0, p) : sm_rowmax64<true>(sr, key0, p);
-        // raw scores; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
-        const float mx = rmax * a.scale_log2;
-        float alpha = 1.f;
-        bool need = false;
-        if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
-          const float m_new = fmaxf(m_run, mx);
-          if (m_run != -INFINITY) { alpha = fast_exp2(m_run - m_new); need = true; }
-          m_run = m_new;
-        }
-        if (__any_sync(0xffffffffu, need)) {  // rare: rebase O_t (PVs up to j-1) and this tile's first-half P
-          if (j > 0) {  // the commit of S_t(j) covered PV_t(j-1): O_t is complete up to j-1
-            uint32_t o[32];
 #pragma unroll 1
-            for (int c = 0; c < DH; c += 32) {
-              tmem_ld32(tmem + lane_base + O_COL + t * 128 + c, o);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st32(tmem + lane_base + O_COL + t * 128 + c, o);
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t sr[64];
+          tmem_ld32(s_col + hh * 64, sr);
+          tmem_ld32(s_col + hh * 64 + 32, sr + 32);
+          tmem_wait_ld();
+          const int key0 = j * BKV + hh * 64;
+          const bool full = key0 + 63 <= p_first;  // every row sees every key of the half: no causal mask
+          uint32_t pk[32];
+          // common case: exps against the running max, no row-max pass at all. Kept unless some row's sum
+          // exceeds 2^64 (then some P > 2^64, or inf/NaN): the half is redone below with the max first.
+          // Any P <= 2^64 keeps O and l finite over 8192 keys, and bf16/fp32 precision is relative.
+          if ((a.debug_mode & 4) == 0 && !__any_sync(0xffffffffu, m_run == -INFINITY)) {
+            const float ls = full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, m_run)
+                                  : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, m_run);
+            if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
+              l_run += ls;
+              tmem_st32(s_col + hh * 32, pk);
+              continue;
             }
           }
-          if (hh == 1) {
-            uint32_t pp[32];
-            tmem_wait_st();
-            tmem_ld32(s_col, pp);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              pp[i] = pack_bf2(__uint_as_float(pp[i] << 16) * alpha, __uint_as_float(pp[i] & 0xFFFF0000u) * alpha);
-            tmem_st32(s_col, pp);
+          const float rmax = full ? sm_rowmax64<false>(sr, key0, p) : sm_rowmax64<true>(sr, key0, p);
+          // raw scores; the softmax scale (> 0) is folded into the max and into one FFMA per exp2
+          const float mx = rmax * a.scale_log2;
+          float alpha = 1.f;
+          bool need = false;
+          if (mx > m_run + RESCALE_THRESHOLD || (m_run == -INFINITY && mx != -INFINITY)) {
+            const float m_new = fmaxf(m_run, mx);
+            if (m_run != -INFINITY) { alpha = fast_exp2(m_run - m_new); need = true; }
+            m_run = m_new;
           }
-          tmem_wait_st();
+          if (__any_sync(0xffffffffu, need)) {  // rare: rebase O_t (PVs up to j-1) and this tile's first-half P
+            if (j > 0) {  // the commit of S_t(j) covered PV_t(j-1): O_t is complete up to j-1
+              uint32_t o[32];
+#pragma unroll 1
+              for (int c = 0; c < DH; c += 32) {
+                tmem_ld32(tmem + lane_base + O_COL + t * 128 + c, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                tmem_st32(tmem + lane_base + O_COL + t * 128 + c, o);
+              }
+            }
+            if (hh == 1) {
+              uint32_t pp[32];
+              tmem_wait_st();
+              tmem_ld32(s_col, pp);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                pp[i] = pack_bf2(__uint_as_float(pp[i] << 16) * alpha, __uint_as_float(pp[i] & 0xFFFF0000u) * alpha);
+              tmem_st32(s_col, pp);
+            }
+            tmem_wait_st();
+          }
+          l_run *= alpha;
+          const float base = (m_run == -INFINITY) ? 0.f : m_run;
+          l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
+                        : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
+          tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)
         }
-        l_run *= alpha;
-        const float base = (m_run == -INFINITY) ? 0.f : m_run;
-        l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
-                      : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
-        tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-    }
-    if (n_t > 0) {
-      mbar_wait(&o_done[t], 0);
+      mbar_wait(&o_done[t], od & 1);
+      ++od;
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      uint16_t* dst = a.o + static_cast<int64_t>(row_start + tt) * H * DH + (kvh * G + g) * DH;
+      uint16_t* dst = a.o + static_cast<int64_t>(row_start + tt) * H * DH + (it.kvh * G + g) * DH;
 #pragma unroll 1
       for (int c = 0; c < DH; c += 32) {
         uint32_t o[32];
         tmem_ld32(tmem + lane_base + O_COL + t * 128 + c, o);
         tmem_wait_ld();
+        if (c + 32 == DH) {  // O_t fully read: the next item's first PV may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_free[t]);
+        }
         if (valid) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
+          for (int i2 = 0; i2 < 32; i2 += 8) {
             uint4 u;
-            u.x = pack_bf2(__uint_as_float(o[i + 0]) * inv, __uint_as_float(o[i + 1]) * inv);
-            u.y = pack_bf2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-            u.z = pack_bf2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-            u.w = pack_bf2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
-            *reinterpret_cast<uint4*>(dst + c + i) = u;
+            u.x = pack_bf2(__uint_as_float(o[i2 + 0]) * inv, __uint_as_float(o[i2 + 1]) * inv);
+            u.y = pack_bf2(__uint_as_float(o[i2 + 2]) * inv, __uint_as_float(o[i2 + 3]) * inv);
+            u.z = pack_bf2(__uint_as_float(o[i2 + 4]) * inv, __uint_as_float(o[i2 + 5]) * inv);
+            u.w = pack_bf2(__uint_as_float(o[i2 + 6]) * inv, __uint_as_float(o[i2 + 7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c + i2) = u;
           }
         }
       }
@@ -290,6 +371,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem, 512);
+  if (threadIdx.x == 0) {  // the last CTA to finish resets the work counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.work_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      a.work_ctr[0] = 0;
+      a.work_ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 }  // namespace
 
@@ -303,8 +392,20 @@ cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, con
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(k_attn_pair, dim3(a.n_tiles / 2, a.n_kv_heads), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV,
-                    a, t_cap);
+  if (a.work_ctr == nullptr) return cudaErrorInvalidValue;
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static const bool persist = [] {
+    const char* e = getenv("RC_ATTN_PERSIST");  // diagnostics: 0 = one CTA per work item
+    return !(e && atoi(e) == 0);
+  }();
+  const int items = a.n_tiles / 2 * a.n_kv_heads;
+  const int grid = persist ? (items < sms ? items : sms) : items;
+  return launch_pdl(k_attn_pair, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV, a, t_cap);
 }
 
 bool attn_use_pairs(int n_tiles, int n_kv_heads, int num_sms) {

@@ -215,6 +215,7 @@ struct rc_ctx {
   float* part_o = nullptr;   // KV-split attention partials
   float* part_ml = nullptr;
   int32_t* part_flag = nullptr;  // adaptive split: which logical tiles were split
+  int32_t* attn_ctr = nullptr;   // paired attention work counter
   size_t part_rows = 0;
   int32_t* sel_pos = nullptr;
   int32_t* sel_dst = nullptr;
@@ -258,7 +259,7 @@ struct rc_ctx {
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
                     a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
-                    mass_lse, mass_a};
+                    mass_lse, mass_a, attn_ctr};
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
@@ -862,6 +863,13 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
     at.split_flag = c->part_flag;
     c->launches += 1;  // the merge kernel
   }
+  if (paired && !c->attn_ctr) {  // persistent paired kernel's work counter (reset by its last CTA)
+    cudaError_t e = cudaSuccess;
+    c->attn_ctr = dev_alloc<int32_t>(2, &e);
+    if (e == cudaSuccess) e = cudaMemset(c->attn_ctr, 0, 2 * sizeof(int32_t));
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "attention work counter");
+  }
+  at.work_ctr = c->attn_ctr;
   if (paired)
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
               attn_pair_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
