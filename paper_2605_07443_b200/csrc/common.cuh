@@ -359,7 +359,9 @@ __device__ __forceinline__ float sm_rowmax64(const uint32_t* sr, int key0, int p
 // P = 2^(s * scale - base) for 64 raw scores, packed as bf16 pairs into pk[32]; returns the sum of
 // the fp32 values. Arithmetic on fp32x2 pairs; 3 chunks of 8 keys in 8 take 2^x on the FMA pipe
 // (poly_exp2 written out on pairs), the rest on the SFU (16 ex2/clk/SM), balancing the two pipes.
-template <bool MASKED>
+// POLY: which 8-key chunks of the 64 take 2^x on the FMA pipe (bit c = chunk c); the kernels pick
+// the split that measured fastest for them (SFU-only for the single-tile kernel, 2 of 8 paired)
+template <bool MASKED, unsigned POLY>
 __device__ __forceinline__ float sm_exp_pack64(const uint32_t* sr, uint32_t* pk, int key0, int p, float scale,
                                                float base) {
   const uint64_t sc2 = f2_pack(scale, scale), nb2 = f2_pack(-base, -base);
@@ -379,7 +381,7 @@ __device__ __forceinline__ float sm_exp_pack64(const uint32_t* sr, uint32_t* pk,
       x1 = (key0 + c + 1 <= p) ? x1 : -INFINITY;
     }
     const int chunk = c >> 3;
-    if (chunk == 2 || chunk == 5 || chunk == 7) {
+    if ((POLY >> chunk) & 1) {
       // clamp to [-127, 65]: no exponent wrap; a speculative base more than 64 below the row max
       // still shows up as P >= 2^65 in the row sum
       const uint64_t xc = f2_pack(fminf(fmaxf(x0, -127.f), 65.f), fminf(fmaxf(x1, -127.f), 65.f));

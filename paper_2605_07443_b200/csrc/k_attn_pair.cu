@@ -38,6 +38,9 @@ constexpr uint32_t OFF_ITEM = OFF_BAR + 256;  // [2] work-item slots (scheduler 
 constexpr uint32_t SMEM_BYTES = OFF_ITEM + 16;
 constexpr uint32_t O_COL = 256;            // O_t at 256 + 128 t
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
+// 2 of 8 key chunks take 2^x on the FMA pipe: measured at cfg3 batch 32, 39.4 ms per step vs 40.3
+// (3 of 8), 42.8 (4 of 8), 40.5 (none)
+constexpr unsigned POLY_CHUNKS = 0x44;
 constexpr float SPEC_SUM_MAX = 18446744073709551616.0f;  // 2^64: bound of the speculative exps' row sum
 constexpr int N_ITEM_CONSUMERS = 2 + 8;    // MMA thread, V producer, 8 softmax warps
 
@@ -285,8 +288,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           // exceeds 2^64 (then some P > 2^64, or inf/NaN): the half is redone below with the max first.
           // Any P <= 2^64 keeps O and l finite over 8192 keys, and bf16/fp32 precision is relative.
           if ((a.debug_mode & 4) == 0 && !__any_sync(0xffffffffu, m_run == -INFINITY)) {
-            const float ls = full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, m_run)
-                                  : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, m_run);
+            const float ls = full ? sm_exp_pack64<false, POLY_CHUNKS>(sr, pk, key0, p, a.scale_log2, m_run)
+                                  : sm_exp_pack64<true, POLY_CHUNKS>(sr, pk, key0, p, a.scale_log2, m_run);
             if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
               l_run += ls;
               tmem_st32(s_col + hh * 32, pk);
@@ -329,8 +332,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           l_run *= alpha;
           const float base = (m_run == -INFINITY) ? 0.f : m_run;
-          l_run += full ? sm_exp_pack64<false>(sr, pk, key0, p, a.scale_log2, base)
-                        : sm_exp_pack64<true>(sr, pk, key0, p, a.scale_log2, base);
+          l_run += full ? sm_exp_pack64<false, POLY_CHUNKS>(sr, pk, key0, p, a.scale_log2, base)
+                        : sm_exp_pack64<true, POLY_CHUNKS>(sr, pk, key0, p, a.scale_log2, base);
           tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)
         }
         tmem_wait_st();
