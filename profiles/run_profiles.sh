@@ -1,6 +1,5 @@
 # Profile capture used for profiles/ (run on the GPU box from the repo root; outputs go to gpurun_out/)
 set -x
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "running_base" > gpurun_out/t_spec.log 2>&1; echo tspec=$?; tail -2 gpurun_out/t_spec.log
 timeout 600 python bench.py > gpurun_out/final_b32.log 2>&1; echo b32=$?
 timeout 600 python bench.py --batch 1 --steps 30 > gpurun_out/final_b1.log 2>&1; echo b1=$?
 python profiles/summ.py gpurun_out/final_b32.log gpurun_out/final_b1.log
