@@ -400,13 +400,21 @@ def run_ours(args, wl):
         hf["ev"][i] = e
         hf["t"].append((a, e))
 
+    fetch_t = []  # (start, end event, items) of every rc_fetch_remote call
+
     def step(i, out=out_bufs):
         b = i % len(batches)
         lay = batches[b]
         if fetch is not None and fetch[b]:  # pull peer-resident candidate items over NVLink (§8(e))
             f = fetch[b]
+            from paper_2605_07443_b200 import _lib as R
+            n_new = int((~ctx.pool_contains(R.RC_POOL_ITEM_BF16, [x[0] for x in f])).sum())  # the ones copied
+            fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            fa.record(stream)
             ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], [x[2] for x in f], [wl.item_len] * len(f),
                              [wl.prefix_len] * len(f), stream=stream)
+            fb.record(stream)
+            fetch_t.append((fa, fb, n_new, len(f)))
         if host_fetch:
             if i not in hf["ev"]:
                 fetch_host(i)
@@ -428,6 +436,7 @@ def run_ours(args, wl):
     clocks = ClockSampler() if rank == 0 else None
     l0 = ctx.launch_count()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    n_fetch_warm = len(fetch_t)
     evs[0].record(stream)
     for i in range(args.steps):
         step(args.warmup + i)
@@ -435,6 +444,26 @@ def run_ours(args, wl):
     torch.cuda.synchronize(device)
     launches = ctx.launch_count() - l0
     step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    item_bytes = wl.item_len * wl.shape.n_layers * 2 * wl.shape.n_kv_heads * wl.shape.head_dim * 2
+    fetch_rep = None
+    if fetch_t:
+        timed = fetch_t[n_fetch_warm:]
+        copied = [(a, e, n) for a, e, n, _ in fetch_t if n > 0]  # warm-up included: later calls hit the LRU
+        f_ms = sum(a.elapsed_time(e) for a, e, _ in copied)
+        f_items = sum(n for _, _, n in copied)
+        fetch_rep = {"items_requested_per_step": sum(m for _, _, _, m in timed) / args.steps,
+                     "items_copied_per_step": sum(n for _, _, n, _ in timed) / args.steps,
+                     "ms_per_step": sum(a.elapsed_time(e) for a, e, _, _ in timed) / args.steps,
+                     "copy_calls": len(copied), "copy_bytes": f_items * item_bytes,
+                     "gbs": f_items * item_bytes / max(f_ms, 1e-9) / 1e6 if copied else None,
+                     "nvlink_peak_gbs": 900.0,
+                     "note": "rc_fetch_remote: one-sided peer reads into the local LRU region; items already "
+                             "resident are skipped, so GB/s is taken over the calls that copied (CUDA events "
+                             "around each call); peak = NVLink 5 per direction"}
+        fetch_rep["frac"] = fetch_rep["gbs"] / fetch_rep["nvlink_peak_gbs"] if copied else None
+        if share:  # every rank on cuda:0: the "peer" pool is on this GPU, the pull is an HBM copy
+            fetch_rep["frac"] = None
+            fetch_rep["note"] += " (RC_BENCH_SHARE_GPU: peer on the same GPU, an HBM copy, not NVLink)"
     total_ms = evs[0].elapsed_time(evs[-1])
     if world > 1:
         dist.barrier()
@@ -529,7 +558,8 @@ def run_ours(args, wl):
         res["shard"] = {"k": world, "edge_cut": sh["cut"], "hot_replicated": int((sh["part"] == -1).sum()),
                         "items_on_rank0": int(sh["res"][0].sum()), "routed_per_rank": sh["routed"],
                         "rank0_local_hit": sh["local_hit"],
-                        "rank0_fetch_items_per_batch": sh.get("fetch_items_per_batch")}
+                        "rank0_fetch_items_per_batch": sh.get("fetch_items_per_batch"),
+                        "rank0_fetch": fetch_rep}
     if world == 1 and not args.no_baselines and not args.profile_only:
         res["baselines"] = baselines(args, wl, env, r_bp, c, step_ms)
     if world == 1 and not args.no_cpu_baseline and not args.profile_only:
