@@ -167,3 +167,24 @@ def test_cfg5_qwen2_8k_batch4_request_matches_oracle():
     print("fullsize cfg5 parity", json.dumps(err))
     assert jac >= 0.8, err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
+
+
+def test_cfg3_batch1_request_matches_oracle():
+    """BASELINE configs[1]/[2] at batch 1 (the TTFT launch configuration: single-tile attention over
+    160 CTAs, 625 Sel rows, residual GEMMs with the RMSNorm fused into their tail for U = 3889 and
+    Sel rows): request 0 end to end against the oracle, same bounds as at batch 32."""
+    wl = rcgen.CFG3
+    res, d = _setup(wl, 1, (0,))
+    r = 0
+    L = d["shape"].n_layers
+    off = res["sel_off"]
+    sel = res["sel_pos"][off[r]:off[r + 1]]
+    lay, K_asm, dfn, forced, own = _oracle(d, r, sel)
+    jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
+    Kg = bf16_to_f32(res["kv_last"][r][0])[sel].astype(np.float64)
+    err = {"jaccard": jac, "logits": rel_l2(res["logits"][r], forced["logits"]),
+           "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
+           "K_last": rel_l2(Kg, forced["K"][L - 1][sel])}
+    print("fullsize cfg3 batch-1 parity", json.dumps(err))
+    assert jac >= 0.8, err
+    assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
