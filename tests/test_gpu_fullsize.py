@@ -169,11 +169,12 @@ def test_cfg5_qwen2_8k_batch4_request_matches_oracle():
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
 
 
-def test_cfg3_batch1_request_matches_oracle():
-    """BASELINE configs[1]/[2] at batch 1 (the TTFT launch configuration: single-tile attention over
-    160 CTAs, 625 Sel rows, residual GEMMs with the RMSNorm fused into their tail for U = 3889 and
-    Sel rows): request 0 end to end against the oracle, same bounds as at batch 32."""
-    wl = rcgen.CFG3
+@pytest.mark.parametrize("wl", [rcgen.CFG3, rcgen.CFG2], ids=["cfg3", "cfg2"])
+def test_batch1_request_matches_oracle(wl):
+    """BASELINE configs[1] (cfg2: 2560-token prompts) and configs[2] (cfg3: 4096) at batch 1, the TTFT
+    launch configuration (single-tile attention over 160 CTAs at cfg3, 395-625 Sel rows on the
+    small-M GEMM schedules, U = 2353-3889 rows in layer 0): request 0 end to end against the oracle,
+    same bounds as at batch 32."""
     res, d = _setup(wl, 1, (0,))
     r = 0
     L = d["shape"].n_layers
@@ -185,6 +186,6 @@ def test_cfg3_batch1_request_matches_oracle():
     err = {"jaccard": jac, "logits": rel_l2(res["logits"][r], forced["logits"]),
            "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
            "K_last": rel_l2(Kg, forced["K"][L - 1][sel])}
-    print("fullsize cfg3 batch-1 parity", json.dumps(err))
+    print(f"fullsize {wl.name} batch-1 parity", json.dumps(err))
     assert jac >= 0.8, err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
