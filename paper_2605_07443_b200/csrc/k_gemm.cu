@@ -275,7 +275,36 @@ __device__ __forceinline__ void epilogue_tile(uint32_t taddr, int m0, int n0, in
 // tile_m rows (128, or 256 for a CTA pair whose rank-1 CTA owns rows row_off = 128 .. 255)
 struct Sched {
   int u0, ustep, units, splits, num_m, num_n, group_m, tile_m, row_off;
+  // stream-K tail (residual epilogue on CTA pairs): tiles [units / splits, +sk_tiles) are cut into
+  // equal k-block ranges, one per cluster, after the whole-tile round-robin part
+  int nk = 0, sk_tiles = 0;
 };
+
+// The it-th work unit of a CTA (cluster): whole tiles / split-K shares round-robin (u0, u0 + ustep,
+// ... < units), then this cluster's k-block range [lo, hi) of the stream-K tail, one unit per tile it
+// crosses. Returns false when the CTA has no more units.
+__device__ __forceinline__ bool unit_at(const Sched& sc, int it, int& tile, int& kb0, int& kb1) {
+  const int n_dp = sc.u0 < sc.units ? (sc.units - sc.u0 + sc.ustep - 1) / sc.ustep : 0;
+  if (it < n_dp) {
+    const int u = sc.u0 + it * sc.ustep;
+    tile = u / sc.splits;
+    const int sp = u % sc.splits;
+    kb0 = sp * sc.nk / sc.splits;
+    kb1 = (sp + 1) * sc.nk / sc.splits;
+    return true;
+  }
+  if (sc.sk_tiles == 0) return false;
+  const int j = it - n_dp;
+  const long long w = static_cast<long long>(sc.sk_tiles) * sc.nk;
+  const long long lo = w * sc.u0 / sc.ustep, hi = w * (sc.u0 + 1) / sc.ustep;
+  const long long st = j == 0 ? lo : (lo / sc.nk + j) * static_cast<long long>(sc.nk);
+  if (st >= hi) return false;
+  const long long t = st / sc.nk;
+  tile = sc.units / sc.splits + static_cast<int>(t);
+  kb0 = static_cast<int>(st - t * sc.nk);
+  kb1 = static_cast<int>(min(static_cast<long long>(sc.nk), hi - t * sc.nk));
+  return true;
+}
 
 // hand an accumulator buffer back to the MMA issuer: every epilogue thread of a single CTA, or one
 // lane per epilogue warp of both CTAs of a pair onto the leader's barrier
@@ -330,10 +359,10 @@ __device__ __forceinline__ void epilogue_loop(uint32_t tmem_base, int warp, int 
     else
       epilogue_heads_loop<BN, 16, EPI, PAIR>(tmem_base, q, M, N, sc, tfull, tempty, leader_tempty, ep);
   } else {
-    int it = 0, chunk_ctr = 0;
+    int chunk_ctr = 0, tile = 0, kb0 = 0, kb1 = 0;
     if (EPI == EPI_ADD_F32 && (threadIdx.x & 31) == 0) tma_prefetch_desc(tmC);
-    for (int u = sc.u0; u < sc.units; u += sc.ustep, ++it) {
-      int mb, nb; tile_coords(u / sc.splits, sc.num_m, sc.num_n, sc.group_m, mb, nb);
+    for (int it = 0; unit_at(sc, it, tile, kb0, kb1); ++it) {
+      int mb, nb; tile_coords(tile, sc.num_m, sc.num_n, sc.group_m, mb, nb);
       const int m0 = mb * sc.tile_m + sc.row_off;
       const int acc = it & 1;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -463,7 +492,7 @@ template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     k_gemm_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, int M, int N, int K, int splits, int group_m,
-                const EpiArgs ep) {
+                int sk_tiles, const EpiArgs ep) {
   using C = PairCfg;
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
@@ -498,19 +527,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
   const int num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
-  const int units = tiles * splits;
+  const int units = (tiles - sk_tiles) * splits;  // round-robin part; the last sk_tiles tiles are stream-K
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const uint32_t leader_full = mapa_shared(full, 0);
   const uint32_t leader_tempty = mapa_shared(tempty, 0);
+  Sched sc{cid, ncl, units, splits, num_m, num_n, group_m, 2 * BM, static_cast<int>(rank) * BM};
+  sc.nk = nk;
+  sc.sk_tiles = sk_tiles;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
-      for (int u = cid; u < units; u += ncl) {
-        int mb, nb; tile_coords(u / splits, num_m, num_n, group_m, mb, nb);
-        const int sp = u % splits;
+      int kb0 = 0, kb1 = 0, tl = 0;
+      for (int it = 0; unit_at(sc, it, tl, kb0, kb1); ++it) {
+        int mb, nb; tile_coords(tl, num_m, num_n, group_m, mb, nb);
         const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
-        for (int kb = sp * nk / splits; kb < (sp + 1) * nk / splits; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
           if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
@@ -523,14 +555,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {  // ---------------- MMA issuer (leader only)
       constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN);
-      int stage = 0; uint32_t phase = 0; int it = 0;
-      for (int u = cid; u < units; u += ncl, ++it) {
+      int stage = 0; uint32_t phase = 0;
+      int tl = 0, kb0 = 0, kb1 = 0;
+      for (int it = 0; unit_at(sc, it, tl, kb0, kb1); ++it) {
         const int acc = it & 1;
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        const int sp = u % splits, kb0 = sp * nk / splits;
-        for (int kb = kb0; kb < (sp + 1) * nk / splits; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
@@ -545,7 +577,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue warps (both CTAs, own 128 rows)
-    const Sched sc{cid, ncl, units, splits, num_m, num_n, group_m, 2 * BM, static_cast<int>(rank) * BM};
     epilogue_loop<BN, EPI, true>(tmem_base, warp, M, N, sc, tfull, tempty, leader_tempty, ep, &tmC, sOut);
   }
   tc_fence_before();
@@ -570,15 +601,23 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   const int num_m = (M + 2 * BM - 1) / (2 * BM);
   const int tiles = num_m * ((N + 255) / 256);
   const int nk = (K + BK - 1) / BK;
-  int splits = 1;
+  int splits = 1, sk_tiles = 0;
   if (EPI == EPI_ADD_F32) {
-    auto cost = [&](int sp) {
-      const int64_t units = static_cast<int64_t>(tiles) * sp;
-      return ((units + pairs - 1) / pairs) * ((nk + sp - 1) / sp + 6);
-    };
-    int64_t best = cost(1);
-    for (int sp = 2; sp <= 16 && nk / sp >= 8; ++sp)
-      if (cost(sp) * 100 < best * 95) { best = cost(sp); splits = sp; }
+    static const bool sk_on = [] { const char* e = std::getenv("RC_GEMM_STREAMK"); return !(e && std::atoi(e) == 0); }();
+    if (sk_on && tiles > pairs && tiles % pairs != 0) {
+      // whole tiles round-robin, the partial last wave cut into equal k-block ranges (the reduce-add
+      // epilogue makes partial tiles free to combine): e.g. cfg3 batch 32, 1264 tiles on 74 pairs =
+      // 17 full waves + 6 tiles spread over all 74 pairs instead of an 18th wave on 6 of them
+      sk_tiles = tiles % pairs;
+    } else {
+      auto cost = [&](int sp) {
+        const int64_t units = static_cast<int64_t>(tiles) * sp;
+        return ((units + pairs - 1) / pairs) * ((nk + sp - 1) / sp + 6);
+      };
+      int64_t best = cost(1);
+      for (int sp = 2; sp <= 16 && nk / sp >= 8; ++sp)
+        if (cost(sp) * 100 < best * 95) { best = cost(sp); splits = sp; }
+    }
   }
   const int units = tiles * splits;
   const int grid = 2 * (units < pairs ? units : pairs);
@@ -589,7 +628,7 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   const int group_m = static_cast<int>(std::max<size_t>(
       2, std::min<size_t>(num_m, group_a_bytes / (static_cast<size_t>(2 * BM) * K * 2))));
   return launch_pdl(k_gemm_pair<EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits,
-                    group_m, ep);
+                    group_m, sk_tiles, ep);
 }
 
 template <int BN, int EPI>
