@@ -113,11 +113,12 @@ def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
     res = cluster.resident_matrix(part, world)
     stream = rcgen.gen_requests(wl, cat, protos, int(1.25 * world * batch * n_batches) + world, start=0)
     routes, _ = cluster.route([r.cand_items.tolist() for r in stream], [wl.n] * len(stream), res)
-    mine = [r for r, p in zip(stream, routes) if p == rank] or stream[rank::world]
+    mine_idx = [k for k, p in enumerate(routes) if p == rank] or list(range(rank, len(stream), world))
+    mine = [stream[k] for k in mine_idx]
     need = batch * n_batches
     reqs = (mine * ((need + len(mine) - 1) // len(mine)))[:need]
     hit = float(np.mean([res[rank][r.cand_items].mean() for r in reqs]))
-    return dict(part=part, cut=cut, res=res, reqs=reqs, local_hit=hit,
+    return dict(part=part, cut=cut, res=res, reqs=reqs, local_hit=hit, mine_idx=mine_idx,
                 routed=[int((routes == p).sum()) for p in range(world)])
 
 
@@ -190,6 +191,7 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_fr
         fetch = [cluster.plan_fetch([r.cand_items for r in reqs[b * batch:(b + 1) * batch]], shard["res"][rank],
                                     directory, rank) for b in range(n_batches)]
         shard["fetch_items_per_batch"] = float(np.mean([len(f) for f in fetch]))
+        shard["directory"] = directory
     host_fetch = None
     if host_items:
         hs = set(host_items)
@@ -631,34 +633,78 @@ def baselines(args, wl, env, r_bp, c, step_ms):
 
 
 def run_poisson(args, wl):
-    """Open-loop Poisson arrivals on one GPU: whenever the device is free, every request that has
+    """Open-loop Poisson arrivals: whenever a GPU is free, every request routed to it that has
     arrived (up to --batch) is assembled and prefilled as one ragged batch; a request's TTFT is the
-    wall-clock time from its arrival to its batch's logits being complete on the device."""
+    wall-clock time from its arrival to its batch's logits being complete on the device. With N > 1
+    ranks (torchrun) one global arrival stream at --poisson-qps is routed by Eq. 2 over the Alg. 1
+    placement (§8(e)); each rank serves its share, pulling peer-resident candidates over NVLink
+    before each batch, and rank 0 reports TTFT percentiles over all requests."""
     import time
     import torch
+    import torch.distributed as dist
     from paper_2605_07443_b200.build import build
-    device = torch.device("cuda", 0)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    share = os.environ.get("RC_BENCH_SHARE_GPU") == "1"
+    if world > 1:
+        dist.init_process_group("gloo" if share else "nccl")
+    device = torch.device("cuda", 0 if share else local)
     torch.cuda.set_device(device)
-    build()
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.barrier()
+
+    def gather(obj):
+        lst = [None] * world
+        dist.all_gather_object(lst, obj)
+        return lst
+
     max_b = args.batch or wl.batch
-    n = args.requests
-    env = build_ours(wl, max_b, (n + max_b - 1) // max_b, 0, device)
+    n_global = args.requests
+    rng = np.random.default_rng(17)
+    arrivals_all = np.cumsum(rng.exponential(1.0 / args.poisson_qps, n_global))
+    if world > 1:
+        # the routed stream: shard_setup draws 1.25 * world * batch * n_batches requests; this rank's
+        # share of the first n_global of them, at their global arrival times
+        nb = (n_global + max_b - 1) // max_b + 1  # room for any routing imbalance (host-side layouts only)
+        env = build_ours(wl, max_b, nb, rank, device, world=world, gather=gather)
+        idx = [k for k in env["shard"]["mine_idx"] if k < n_global]
+        arrivals = arrivals_all[idx]
+    else:
+        env = build_ours(wl, max_b, (n_global + max_b - 1) // max_b, 0, device)
+        idx = list(range(n_global))
+        arrivals = arrivals_all
+    n = len(idx)
     ctx = env["ctx"]
     lays = [l for b in env["batches"] for l in b][:n]
+    reqs = env["reqs"][:n]
     r_bp, c = args.r_bp or wl.r_bp, args.check_layer
     stream = torch.cuda.current_stream(device)
-    rng = np.random.default_rng(17)
-    arrivals = np.cumsum(rng.exponential(1.0 / args.poisson_qps, n))
+    fetched = []
 
-    def serve(batch_lays):
+    def serve(batch_ids):
+        batch_lays = [lays[r] for r in batch_ids]
+        if world > 1:  # pull the batch's peer-resident candidates over NVLink (§8(e))
+            from paper_2605_07443_b200 import cluster
+            f = cluster.plan_fetch([reqs[r].cand_items for r in batch_ids], env["shard"]["res"][rank],
+                                   env["shard"]["directory"], rank)
+            if f:
+                ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], [x[2] for x in f], [wl.item_len] * len(f),
+                                 [wl.prefix_len] * len(f), stream=stream)
+            fetched.append(len(f))
         seqs = ctx.assemble(batch_lays, prefix_id=1, gather_from=c, stream=stream)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False,
                               n_cand=sum(len(l["cand_idtok"]) for l in batch_lays), stream=stream)
         ctx.release(seqs)
 
-    for k in range(3):  # warm-up at the largest batch
-        serve(lays[:max_b])
+    for k in range(3 if n > 0 else 0):  # warm-up at the largest batch
+        serve(list(range(min(max_b, n))))
     torch.cuda.synchronize(device)
+    fetched.clear()
+    if world > 1:
+        dist.barrier()
     ttft, sizes = np.zeros(n), []
     i, queue = 0, []
     t0 = time.perf_counter()
@@ -672,7 +718,7 @@ def run_poisson(args, wl):
             time.sleep(max(0.0, arrivals[i] - (time.perf_counter() - t0)))
             continue
         batch, queue = queue[:max_b], queue[max_b:]
-        serve([lays[r] for r in batch])
+        serve(batch)
         torch.cuda.synchronize(device)
         t_done = time.perf_counter() - t0
         for r in batch:
@@ -680,13 +726,32 @@ def run_poisson(args, wl):
         sizes.append(len(batch))
         done += len(batch)
     span = time.perf_counter() - t0
-    out = {"metric": METRIC, "mode": "poisson", "qps": args.poisson_qps, "requests": n, "max_batch": max_b,
-           "config": {"workload": wl.name, "seq_len": wl.n, "r": r_bp / 1e4, "check_layer": c},
-           "ttft_ms": {"p50": float(np.percentile(ttft, 50, method="inverted_cdf")),
-                       "p99": float(np.percentile(ttft, 99, method="inverted_cdf")), "mean": float(ttft.mean())},
-           "served_tok_s": n * wl.n / span, "batches": len(sizes), "mean_batch": float(np.mean(sizes)),
-           "timing": "wall clock: arrival (seeded exponential gaps) -> device synchronize after the batch's LM head"}
-    print(json.dumps(out))
+    per_rank = {"rank": rank, "requests": n, "span_s": span, "batches": len(sizes),
+                "mean_batch": float(np.mean(sizes)) if sizes else 0.0,
+                "fetch_items_per_batch": float(np.mean(fetched)) if fetched else 0.0}
+    if world > 1:
+        parts = gather((ttft.tolist(), per_rank))
+        all_ttft = np.array([t for p in parts for t in p[0]])
+        ranks = [p[1] for p in parts]
+        span = max(r["span_s"] for r in ranks)
+    else:
+        all_ttft, ranks = ttft, [per_rank]
+    if rank == 0:
+        out = {"metric": METRIC, "mode": "poisson", "qps": args.poisson_qps, "requests": int(len(all_ttft)),
+               "n_gpus": world, "max_batch": max_b,
+               "config": {"workload": wl.name, "seq_len": wl.n, "r": r_bp / 1e4, "check_layer": c,
+                          "routing": "Eq. 2 over the Alg. 1 placement" if world > 1 else "single GPU"},
+               "ttft_ms": {"p50": float(np.percentile(all_ttft, 50, method="inverted_cdf")),
+                           "p99": float(np.percentile(all_ttft, 99, method="inverted_cdf")),
+                           "mean": float(all_ttft.mean())},
+               "served_tok_s": len(all_ttft) * wl.n / span, "per_rank": ranks,
+               "timing": "wall clock: arrival (seeded exponential gaps) -> device synchronize after the batch's "
+                         "LM head; percentiles over every request of every rank"}
+        if share:
+            out["note"] = "RC_BENCH_SHARE_GPU: all ranks on one GPU (exercises the path; not a scaling number)"
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
     ctx.close()
 
 
