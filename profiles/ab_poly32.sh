@@ -1,3 +1,5 @@
+# A/B of the paired kernel's POLY_CHUNKS (build each variant first: set POLY_CHUNKS in k_attn_pair.cu, build,
+# copy paper_2605_07443_b200/librc.so to build/variants/librc_<mask>.so), batch-32 bench lines per variant
 set -x
 for rep in 1 2; do for v in 0x44 0x10 0x11; do
   cp build/variants/librc_$v.so paper_2605_07443_b200/librc.so
