@@ -136,31 +136,43 @@ def test_selective_r100_equals_full(wl):
 
 @pytest.mark.parametrize("c", [0, 1])
 def test_selective_r0_equals_hf_tail_over_stitched_cache(c):
+    # r = 0: Sel is exactly the FORCED tail. c = 0: the tail attends over the stitched KV at
+    # every layer. c = 1: layer 0 is recomputed for all of U (R12), so the tail's layer-0 context
+    # is the prefix cache + the fresh layer-0 K/V of U -- which depend only on (token, position),
+    # so HF's own full forward supplies them -- and layers >= 1 are the stitched KV.
     wl = rcgen.CFG1
     case, m, pools, lay = _tiny_setup(wl, exact_prefix=False)
     s = case["shape"]
-    K, V, _ = assemble(s, lay, pools["items"], pools["hist"], pools["prefix"], gather_from=0)
+    K, V, _ = assemble(s, lay, pools["items"], pools["hist"], pools["prefix"], gather_from=c)
     sel = selective_prefill(m, lay, K, V, 0, 0, check_layer=c)
     T = wl.tail_len
     n = lay.n
-    assert list(sel["sel"]) == list(range(n - T, n)) if c == 0 else True
-    if c != 0:
-        return
-    # library routine: HF forward of the tail with past_key_values = stitched KV[0..n-T)
+    P = wl.prefix_len
+    assert list(sel["sel"]) == list(range(n - T, n))
+    # library routine: HF forward of the tail with past_key_values = that context
     from transformers import DynamicCache
     hf = hf_model(s, case["W"])
+    _, kv_full = _hf_logits_and_kv(hf, lay.tokens.tolist())
     cache = DynamicCache(config=hf.config)
     for l in range(s.n_layers):
         k = torch.from_numpy(bf16_to_f32(K[l][:n - T])).permute(1, 0, 2)[None]
         v = torch.from_numpy(bf16_to_f32(V[l][:n - T])).permute(1, 0, 2)[None]
+        if l < c:   # fresh layer-0 K/V of U from HF's own forward of the whole prompt
+            k[:, :, P:] = kv_full.layers[l].keys[:, :, P:n - T]
+            v[:, :, P:] = kv_full.layers[l].values[:, :, P:n - T]
         cache.update(k, v, l)
     with torch.no_grad():
         out = hf(torch.tensor([lay.tokens[n - T:].tolist()]), past_key_values=cache,
                  position_ids=torch.arange(n - T, n)[None], use_cache=True)
     assert rel_l2(sel["logits"], out.logits[0, -1].double().numpy()) < 2e-5
-    # non-forced positions keep their stitched bytes at every layer
+    # non-forced positions keep their stitched bytes at every layer >= c; layers < c hold the
+    # fresh K of U (HF's values, to fp32 rounding)
     for l in range(s.n_layers):
-        assert np.array_equal(bf16_bits(sel["K"][l][:n - T].astype(np.float32)), K[l][:n - T])
+        if l >= c:
+            assert np.array_equal(bf16_bits(sel["K"][l][:n - T].astype(np.float32)), K[l][:n - T])
+        else:
+            k_hf = kv_full.layers[l].keys[0].permute(1, 0, 2).double().numpy()
+            assert rel_l2(sel["K"][l][P:n], k_hf[P:n]) < 2e-5
 
 
 @pytest.mark.parametrize("r_bp,c,lam", [(0, 1, 1.0), (1500, 1, 1.0), (1500, 0, 1.0), (5000, 1, 1.0),

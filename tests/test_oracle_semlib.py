@@ -59,7 +59,13 @@ def test_match_self_and_exact_nn_among_candidates():
         assert np.array_equal(lib.C[pid], lib.C[i]) and pid <= i and abs(cos - 1.0) < 1e-6
     hits = 0
     for q in range(60):  # the exact NN wins whenever it is among the LSH candidates
-        tok, off = int(rng.integers(0, 5000)), int(rng.integers(0, 640))
+        if q % 2 == 0:   # a prototype's token at another offset of its bucket: same embedding
+            i = int(rng.integers(0, 300))
+            b = bucket(int(offs[i]), 10)
+            tok, off = int(toks[i]), int(rng.integers(2 ** b - 1, min(2 ** (b + 1) - 1, 640)))
+            assert bucket(off, 10) == b
+        else:            # an unrelated (token, offset)
+            tok, off = int(rng.integers(0, 5000)), int(rng.integers(0, 640))
         v = embed(tok, off, 10, SEED)
         exact = dot_rows(np.broadcast_to(v, lib.C.shape), lib.C)
         nn = int(np.argmax(exact))
@@ -73,7 +79,7 @@ def test_match_self_and_exact_nn_among_candidates():
             same = np.nonzero(lib.bucket == bucket(off, 10))[0]
             pool = same if len(same) else np.arange(len(lib.C))
             assert pid == int(pool[np.argmax(exact[pool])])
-    assert hits >= 0
+    assert hits >= 30   # every same-embedding query hashes into its prototype's buckets
 
 
 def test_positional_code_values():
