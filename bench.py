@@ -187,7 +187,7 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_fr
         handle, rows = ctx.pool_export()
         peers = [x for x in gather((rank, device.index, handle, rows)) if x[0] != rank]
         ctx.peer_attach([p[0] for p in peers], [p[1] for p in peers], [p[2] for p in peers], [p[3] for p in peers])
-        directory = cluster.exchange_directory(items, ctx.pool_locate(items), rank, gather)
+        directory = cluster.share_directory(ctx, rank, gather)
         fetch = [cluster.plan_fetch([r.cand_items for r in reqs[b * batch:(b + 1) * batch]], shard["res"][rank],
                                     directory, rank) for b in range(n_batches)]
         shard["fetch_items_per_batch"] = float(np.mean([len(f) for f in fetch]))
@@ -413,8 +413,7 @@ def run_ours(args, wl):
             n_new = int((~ctx.pool_contains(R.RC_POOL_ITEM_BF16, [x[0] for x in f])).sum())  # the ones copied
             fa, fb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             fa.record(stream)
-            ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], [x[2] for x in f], [wl.item_len] * len(f),
-                             [wl.prefix_len] * len(f), stream=stream)
+            ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], stream=stream)
             fb.record(stream)
             fetch_t.append((fa, fb, n_new, len(f)))
         if host_fetch:
@@ -691,8 +690,7 @@ def run_poisson(args, wl):
             f = cluster.plan_fetch([reqs[r].cand_items for r in batch_ids], env["shard"]["res"][rank],
                                    env["shard"]["directory"], rank)
             if f:
-                ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], [x[2] for x in f], [wl.item_len] * len(f),
-                                 [wl.prefix_len] * len(f), stream=stream)
+                ctx.fetch_remote([x[0] for x in f], [x[1] for x in f], stream=stream)
             fetched.append(len(f))
         seqs = ctx.assemble(batch_lays, prefix_id=1, gather_from=c, stream=stream)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False,

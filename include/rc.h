@@ -49,7 +49,9 @@ enum { RC_POOL_ITEM_BF16 = 0, RC_POOL_HIST_INT8 = 1, RC_POOL_PREFIX_BF16 = 2, RC
 enum { RC_TOK_PREFIX = 0, RC_TOK_FORCED = 1, RC_TOK_HIST = 2, RC_TOK_ITEM = 3 };
 enum { RC_MISS_ERROR = 0, RC_MISS_RECOMPUTE = 1 };
 
-/* Decoder shape (Llama / Qwen2 family). head_dim in {16, 64, 128}; d_model <= 8192. */
+/* Decoder shape (Llama / Qwen2 family). head_dim in {16, 64, 128}; d_model <= 8192;
+ * 2*n_kv_heads*head_dim <= 2048 (the R4 deviation of a token sums that many fixed-point terms and
+ * must stay below 2^51 for the R6 selection key), else rc_create fails with INVALID. */
 typedef struct rc_model_desc {
   int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
   double rope_theta; /* RoPE base (rotate-half pairs) */
@@ -166,7 +168,9 @@ rc_status rc_decompose_prompt(const rc_prompt* pr, int32_t cap, int32_t* n_out, 
  * for HIST (per token/layer/K-V/kv-head, R15), else NULL. HIST blocks are single tokens
  * (prototypes, n_tokens = 1). PREFIX blocks must have canon_pos = 0. Copies on `stream`;
  * the caller may free kv/scales after the stream passes this point. All-or-nothing.
- * Errors: EXISTS (duplicate id), CAPACITY (pool full), INVALID (kind / shape). */
+ * Canonical positions must lie inside one prompt: 0 <= canon_pos[i] and canon_pos[i] + n_tokens[i]
+ * <= max_seq_len (the alignment offset indexes the RoPE table over [-max_seq_len, max_seq_len]).
+ * Errors: EXISTS (duplicate id), CAPACITY (pool full), INVALID (kind / shape / positions). */
 rc_status rc_pool_register_blocks(rc_ctx* ctx, int32_t kind, int32_t n_blocks, const uint64_t* block_ids,
                                   const int32_t* n_tokens, const int32_t* canon_pos, const void* kv,
                                   const float* scales, rc_stream stream);
@@ -201,7 +205,9 @@ rc_status rc_sel_count(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_
  *   cand_scores f32 [sum n_cand]            logits[cand_idtok] (R19), request-major
  *   sel_pos     i32 [sum |Sel|]             selected positions, ascending per request
  *   hidden      f32 [sum |Sel|][d]          x_L at Sel (before the final norm, R20)
- * Errors: INVALID (params, c < gather_from of a sequence, forced_sel malformed),
+ * Position n-1 must be recomputed (its logits are the output): FORCED, or inside the window.
+ * Errors: INVALID (params, c < gather_from of a sequence, forced_sel malformed, last position
+ * neither FORCED nor in the window),
  * UNSUPPORTED (lambda < 1 with head_dim != 128), CAPACITY (sum n > max_batch_tokens),
  * NOMEM (attention-mass workspace on first lambda < 1 call), NOTFOUND (seq). */
 rc_status rc_selective_prefill(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,
@@ -238,13 +244,29 @@ rc_status rc_pool_export(rc_ctx* ctx, void* ipc_handle_out, int64_t* pool_rows_o
  * rc_fetch_remote; a handle equal to this context's own export maps loopback. */
 rc_status rc_peer_attach(rc_ctx* ctx, int32_t n_peers, const int32_t* peer_rank, const int32_t* peer_device,
                          const void* const* ipc_handles, const int64_t* pool_rows);
+/* This pool's own item blocks (not remote-cache copies) for publishing to peers: up to `cap`
+ * entries of (id, first pool row, n_tokens, canonical start); *n_out = the total count.
+ * Pass cap = 0 to query the size. Errors: CAPACITY (cap < count; n_out still set). */
+rc_status rc_pool_list(rc_ctx* ctx, int32_t cap, uint64_t* item_ids, int64_t* pool_rows, int32_t* n_tokens,
+                       int32_t* canon_pos, int32_t* n_out);
+/* Load an attached peer's item directory (its rc_pool_list, exchanged by the caller through
+ * torch.distributed), replacing any earlier one for that rank. Host arrays, copied. Every entry
+ * must lie inside the peer's pool rows and the position range. All-or-nothing.
+ * Errors: PEER (rank not attached), INVALID (entry out of range). */
+rc_status rc_peer_directory(rc_ctx* ctx, int32_t peer_rank, int32_t n, const uint64_t* item_ids,
+                            const int64_t* pool_rows, const int32_t* n_tokens, const int32_t* canon_pos);
 /* Pull item blocks from their owners' pools over NVLink into this context's remote-cache
- * region (LRU, library-owned) and make them resident here (the beyond-paper replacement of
- * "cache misses are computed on-the-fly"). owner_row = the item's first pool row
- * on the owner (from the owner's rc_pool_locate). Already-resident ids are skipped.
- * Errors: PEER (rank not attached), CAPACITY (remote region too small for one call). */
+ * region and make them resident here (the beyond-paper replacement of "cache misses are
+ * computed on-the-fly"). owner_rank[i] = the attached peer holding
+ * item_ids[i]; rows, lengths and canonical positions come from that peer's directory
+ * (rc_peer_directory). Already-resident and repeated ids are skipped. The region is an LRU
+ * cache: blocks not used by this call may be evicted (least recently used first; rc_assemble
+ * and fetches mark use), planned on the host before any state changes; then ONE batched copy
+ * kernel (one-sided peer reads, 16-byte vectors) moves every block on `stream`. Ordering: the
+ * caller orders a fetch after the rc_assemble calls that read blocks it may evict.
+ * Errors: PEER (rank not attached), NOTFOUND (id not in the owner's directory), CAPACITY (the
+ * blocks of one call exceed the region) -- with no partial effects. */
 rc_status rc_fetch_remote(rc_ctx* ctx, int32_t n_items, const uint64_t* item_ids, const int32_t* owner_rank,
-                          const int64_t* owner_row, const int32_t* n_tokens, const int32_t* canon_pos,
                           rc_stream stream);
 /* Host tier (the paper's CPU-resident item cache with its PCIe transfer,
  * PAPER.md:551, 566): copy item blocks registered with RC_POOL_ITEM_HOST_BF16 into this
@@ -290,6 +312,14 @@ rc_status rc_profile_end(rc_ctx* ctx, int32_t n_kinds, double* ms, int64_t* coun
 /* ---------------------------------------------------------------- diagnostics (tests) */
 /* Stitched KV of one layer of a sequence -> DEVICE bf16 k_out/v_out [n][H_kv][d_h]. */
 rc_status rc_seq_read_kv(rc_ctx* ctx, rc_seq seq, int32_t layer, void* k_out, void* v_out, rc_stream stream);
+/* Pool materialisation ("precomputes their KV blocks
+ * offline"): the stitched KV of positions pos0 .. pos0+n_tok-1 of a sequence (typically after a
+ * full prefill, r = 100%) -> DEVICE kv_out in the registration layout [n_tok][L][2][H_kv][d_h]:
+ * bf16 (int8 = 0), or int8 codes with DEVICE scales_out f32 [n_tok][L][2][H_kv] quantised by R15
+ * (scale = absmax/127 per token, layer, K/V and kv-head; q = clamp(rint_even(x/scale), -127, 127)).
+ * Async on `stream`. Errors: NOTFOUND (seq), INVALID (range). */
+rc_status rc_seq_export_kv(rc_ctx* ctx, rc_seq seq, int32_t pos0, int32_t n_tok, int32_t int8, void* kv_out,
+                           float* scales_out, rc_stream stream);
 /* K5+K6 unit path on given bf16 operands (DEVICE): D[i] = sum |a - b| in the R4 fixed point
  * over `width` elements of K and V, then the selection of rc_selective_prefill for one request
  * whose U rows are these n_u tokens (classes cls, positions P..P+n_u-1). Outputs: dev_out

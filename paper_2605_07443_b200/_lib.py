@@ -92,11 +92,14 @@ def lib():
             "rc_release": (None, [P, C.c_int32, U64P]),
             "rc_pool_export": (C.c_int32, [P, P, I64P]),
             "rc_peer_attach": (C.c_int32, [P, C.c_int32, I32P, I32P, PP, I64P]),
-            "rc_fetch_remote": (C.c_int32, [P, C.c_int32, U64P, I32P, I64P, I32P, I32P, P]),
+            "rc_fetch_remote": (C.c_int32, [P, C.c_int32, U64P, I32P, P]),
+            "rc_pool_list": (C.c_int32, [P, C.c_int32, U64P, I64P, I32P, I32P, I32P]),
+            "rc_peer_directory": (C.c_int32, [P, C.c_int32, C.c_int32, U64P, I64P, I32P, I32P]),
             "rc_fetch_host": (C.c_int32, [P, C.c_int32, U64P, P]),
             "rc_semlib_build": (C.c_int32, [P, C.c_int32, I32P, I32P, C.c_int32, C.POINTER(C.c_float), C.c_uint64]),
             "rc_semlib_match": (C.c_int32, [P, C.c_int32, P, P, P, P, P]),
             "rc_seq_read_kv": (C.c_int32, [P, C.c_uint64, C.c_int32, P, P, P]),
+            "rc_seq_export_kv": (C.c_int32, [P, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, P, P, P]),
             "rc_diag_deviation_select": (C.c_int32, [C.c_int32, C.c_int32, P, P, P, P, U8P, C.c_int32, C.c_int32,
                                                      C.c_int32, C.c_int32, P, P, I32P, P]),
             "rc_diag_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int32, P]),
@@ -131,5 +134,6 @@ EXPORTED = ["rc_create", "rc_destroy", "rc_last_error", "rc_abi_version", "rc_de
             "rc_pool_register_blocks", "rc_pool_contains", "rc_pool_locate", "rc_assemble", "rc_sel_count",
             "rc_selective_prefill", "rc_release", "rc_pool_export", "rc_peer_attach", "rc_fetch_remote",
             "rc_seq_read_kv", "rc_diag_deviation_select", "rc_diag_gemm", "rc_launch_count", "rc_profile_begin",
-            "rc_profile_end", "rc_place_items", "rc_route", "rc_fetch_host", "rc_semlib_build", "rc_semlib_match"]
+            "rc_profile_end", "rc_place_items", "rc_route", "rc_fetch_host", "rc_semlib_build", "rc_semlib_match",
+            "rc_pool_list", "rc_peer_directory", "rc_seq_export_kv"]
 KINDS = ["gemm", "attention", "gather", "select", "small", "lm_head", "fetch"]

@@ -50,6 +50,7 @@ class RcContext:
         check(lib().rc_create(C.byref(md), C.byref(w), C.byref(pd), device, C.byref(out)))
         self.ctx = out
         self.max_batch_tokens = max_batch_tokens
+        self.arena_rows = arena_rows
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -187,6 +188,18 @@ class RcContext:
         check(lib().rc_seq_read_kv(self.ctx, int(seq), layer, _dptr(k), _dptr(v), _stream(stream)))
         return k, v
 
+    def export_kv(self, seq, pos0, n_tok, int8=False, stream=None):
+        """rc_seq_export_kv: positions pos0.. of a sequence -> registration layout [n][L][2][Hk][dh]
+        (bf16, or int8 codes + fp32 scales [n][L][2][Hk] per R15)."""
+        s = self.shape
+        dev = torch.device("cuda", self.device)
+        shp = (n_tok, s.n_layers, 2, s.n_kv_heads, s.head_dim)
+        kv = torch.empty(shp, dtype=torch.int8 if int8 else torch.bfloat16, device=dev)
+        sc = torch.empty(shp[:4], dtype=torch.float32, device=dev) if int8 else None
+        check(lib().rc_seq_export_kv(self.ctx, int(seq), int(pos0), int(n_tok), 1 if int8 else 0, _dptr(kv),
+                                     _dptr(sc) if sc is not None else None, _stream(stream)))
+        return (kv, sc) if int8 else kv
+
     def release(self, seqs):
         seqs = np.ascontiguousarray(seqs, np.uint64)
         lib().rc_release(self.ctx, len(seqs), np_ptr(seqs, C.c_uint64))
@@ -221,16 +234,33 @@ class RcContext:
         check(lib().rc_peer_attach(self.ctx, n, np_ptr(r, C.c_int32), np_ptr(d, C.c_int32), C.cast(hp, R.PP),
                                    np_ptr(rw, C.c_int64)))
 
-    def fetch_remote(self, item_ids, owner_rank, owner_row, n_tokens, canon_pos, stream=None):
-        ids = np.ascontiguousarray(item_ids, np.uint64)
-        o = np.ascontiguousarray(owner_rank, np.int32)
-        orow = np.ascontiguousarray(owner_row, np.int64)
+    def pool_list(self):
+        """rc_pool_list: this pool's own item blocks -> (ids, rows, n_tokens, canon_pos)."""
+        n = C.c_int32()
+        lib().rc_pool_list(self.ctx, 0, None, None, None, None, C.byref(n))
+        ids = np.zeros(n.value, np.uint64)
+        rows = np.zeros(n.value, np.int64)
+        nt = np.zeros(n.value, np.int32)
+        cp = np.zeros(n.value, np.int32)
+        check(lib().rc_pool_list(self.ctx, n.value, np_ptr(ids, C.c_uint64), np_ptr(rows, C.c_int64),
+                                 np_ptr(nt, C.c_int32), np_ptr(cp, C.c_int32), C.byref(n)))
+        return ids, rows, nt, cp
+
+    def peer_directory(self, peer_rank, ids, rows, n_tokens, canon_pos):
+        """rc_peer_directory: load an attached peer's item directory (from its pool_list)."""
+        ids = np.ascontiguousarray(ids, np.uint64)
+        rows = np.ascontiguousarray(rows, np.int64)
         nt = np.ascontiguousarray(n_tokens, np.int32)
         cp = np.ascontiguousarray(canon_pos, np.int32)
-        check(lib().rc_fetch_remote(self.ctx, len(ids), np_ptr(ids, C.c_uint64), np_ptr(o, C.c_int32),
-                                    np_ptr(orow, C.c_int64), np_ptr(nt, C.c_int32), np_ptr(cp, C.c_int32),
-                                    _stream(stream)))
+        check(lib().rc_peer_directory(self.ctx, int(peer_rank), len(ids), np_ptr(ids, C.c_uint64),
+                                      np_ptr(rows, C.c_int64), np_ptr(nt, C.c_int32), np_ptr(cp, C.c_int32)))
 
+    def fetch_remote(self, item_ids, owner_rank, stream=None):
+        """rc_fetch_remote: pull item blocks from their owners' pools (one batched NVLink copy)."""
+        ids = np.ascontiguousarray(item_ids, np.uint64)
+        o = np.ascontiguousarray(owner_rank, np.int32)
+        check(lib().rc_fetch_remote(self.ctx, len(ids), np_ptr(ids, C.c_uint64), np_ptr(o, C.c_int32),
+                                    _stream(stream)))
 
     def fetch_host(self, item_ids, stream=None):
         """rc_fetch_host: host-tier item blocks -> the HBM remote-cache region on the copy engines."""

@@ -77,6 +77,19 @@ def exchange_directory(local_items, local_rows, rank, all_gather_object):
     return directory
 
 
+def share_directory(ctx, rank, all_gather_object):
+    """Publish this rank's pool directory (rc_pool_list) and load every other rank's into the
+    library (rc_peer_directory), so rc_fetch_remote resolves rows from (item id, owner) alone.
+    Returns the global item -> (owner rank, pool row) map (first owner by rank order)."""
+    ids, rows, nt, cp = ctx.pool_list()
+    gathered = all_gather_object({"rank": rank, "ids": ids, "rows": rows, "nt": nt, "cp": cp})
+    for g in gathered:
+        if g["rank"] != rank:
+            ctx.peer_directory(g["rank"], g["ids"], g["rows"], g["nt"], g["cp"])
+    return exchange_directory(ids, rows, rank, lambda _: [{"rank": g["rank"], "items": dict(
+        zip(g["ids"].tolist(), g["rows"].tolist()))} for g in gathered])
+
+
 def plan_fetch(batch_candidates, resident_local, directory, rank):
     """Items of the batch not resident on this rank -> list of (item, owner, row). Raises if an
     item has no owner (it would become FORCED under RC_MISS_RECOMPUTE instead)."""

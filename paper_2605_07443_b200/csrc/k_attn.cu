@@ -212,12 +212,7 @@ __global__ void __launch_bounds__(128) k_attn(const AttnArgs a) {
 template <int DH>
 cudaError_t launch(const AttnArgs& a, cudaStream_t s) {
   using C = AttnCfg<DH>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_attn<DH>), C::SMEM); e != cudaSuccess) return e;
   dim3 grid(a.n_tiles, a.n_kv_heads);
   return launch_pdl(k_attn<DH>, dim3(grid), dim3(128), C::SMEM, s, a);
 }

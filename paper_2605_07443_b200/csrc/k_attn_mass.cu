@@ -167,12 +167,7 @@ __global__ void k_mass_combine(unsigned long long* __restrict__ dev, const unsig
 cudaError_t attn_mass_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const MassArgs& a, int64_t t_cap,
                              cudaStream_t s) {
   if (a.n_key_tiles <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_mass, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_attn_mass), SMEM_BYTES); e != cudaSuccess) return e;
   return launch_pdl(k_attn_mass, dim3(a.n_key_tiles, a.n_kv_heads), dim3(256), SMEM_BYTES, s, *tmQ, *tmK, a, t_cap);
 }
 

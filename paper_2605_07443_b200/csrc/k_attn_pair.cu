@@ -389,12 +389,7 @@ cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, con
                              const AttnArgs& a, int64_t t_cap, cudaStream_t s) {
   if (a.n_tiles <= 0) return cudaSuccess;
   if (a.n_tiles % 2 != 0 || a.head_dim != DH || a.n_splits != 1) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_attn_pair), SMEM_BYTES); e != cudaSuccess) return e;
   if (a.work_ctr == nullptr) return cudaErrorInvalidValue;
   static const int sms = [] {
     int dev = 0, n = 148;

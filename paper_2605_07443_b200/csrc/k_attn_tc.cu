@@ -358,12 +358,7 @@ int attn_tc_tokens_per_tile(int group) { return ROWS / group; }
 cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV, const AttnArgs& a,
                            int64_t t_cap, cudaStream_t s) {
   if (a.n_tiles <= 0) return cudaSuccess;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_attn_tc), SMEM_BYTES); e != cudaSuccess) return e;
   dim3 grid(a.n_tiles, a.n_kv_heads);
   cudaError_t e = launch_pdl(k_attn_tc, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV, a, t_cap);
   if (e != cudaSuccess || a.n_splits <= 1) return e;

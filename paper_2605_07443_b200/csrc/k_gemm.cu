@@ -591,12 +591,7 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
                         const EpiArgs& ep, int num_sms, cudaStream_t s) {
   if (EPI == EPI_ADD_F32 && c == nullptr) return cudaErrorInvalidValue;
   using C = PairCfg;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm_pair<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_gemm_pair<EPI>), C::SMEM); e != cudaSuccess) return e;
   const int pairs = num_sms / 2;
   const int num_m = (M + 2 * BM - 1) / (2 * BM);
   const int tiles = num_m * ((N + 255) / 256);
@@ -636,12 +631,7 @@ cudaError_t launch_one(const CUtensorMap* a, const CUtensorMap* b, const CUtenso
                        const EpiArgs& ep, int num_sms, cudaStream_t s) {
   if (EPI == EPI_ADD_F32 && c == nullptr) return cudaErrorInvalidValue;
   using C = GemmCfg<BN>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(k_gemm<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
-  if (attr_err != cudaSuccess) return attr_err;
+  if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_gemm<BN, EPI>), C::SMEM); e != cudaSuccess) return e;
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int nk = (K + BK - 1) / BK;
   // split-K for additive epilogues when the tile count fills the SMs badly: pick the split that

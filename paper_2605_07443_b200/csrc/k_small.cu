@@ -251,6 +251,59 @@ __global__ void k_copy_rows(const uint8_t* __restrict__ src, int64_t src_rows, i
   }
 }
 
+// one grid row per segment (blockIdx.y), 16-byte units grid-strided over its planes x rows
+__global__ void k_copy_segments(const CopySeg* __restrict__ segs, uint8_t* __restrict__ dst, int64_t dst_rows,
+                                int32_t planes, int32_t row_bytes) {
+  griddep_wait();  // PDL: the segment table (H2D) and earlier kernels are complete and visible
+  griddep_launch();
+  const CopySeg sg = segs[blockIdx.y];
+  const uint8_t* src = static_cast<const uint8_t*>(sg.src);
+  const int cpr = row_bytes / 16;
+  const int64_t per_plane = static_cast<int64_t>(sg.n_rows) * cpr;
+  const int64_t units = per_plane * planes;
+  for (int64_t u = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; u < units;
+       u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t plane = u / per_plane;
+    const int64_t rc = u - plane * per_plane;
+    const int64_t r = rc / cpr;
+    const int c = static_cast<int>(rc - r * cpr);
+    const uint4 v = *reinterpret_cast<const uint4*>(src + (plane * sg.src_rows + sg.src_row0 + r) * row_bytes + c * 16);
+    *reinterpret_cast<uint4*>(dst + (plane * dst_rows + sg.dst_row0 + r) * row_bytes + c * 16) = v;
+  }
+}
+
+// Pool materialisation (R16/R17): stitched rows [row0, row0+n) of every plane -> the registration
+// layout [n][L][2][Hk][dh] (bf16 copy), or int8 codes + fp32 scales per (token, layer, K/V, head) with
+// the R15 rule: scale = absmax/127 (fp32), q = clamp(rint_even(x / scale), -127, 127), scale 0 -> q 0.
+// One warp per (token, plane) row.
+__global__ void k_export_kv(const uint16_t* __restrict__ arena, int64_t arena_rows, int32_t planes, int32_t dh,
+                            int32_t row0, int32_t n, int32_t int8, void* __restrict__ out, float* __restrict__ scales) {
+  griddep_wait();
+  griddep_launch();
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  if (w >= static_cast<int64_t>(n) * planes) return;
+  const int64_t t = w / planes;
+  const int plane = static_cast<int>(w - t * planes);
+  const uint16_t* src = arena + (static_cast<int64_t>(plane) * arena_rows + row0 + t) * dh;
+  const int64_t o = (t * planes + plane) * dh;  // [t][l][kv][h][dh] == [t][plane][dh]
+  if (!int8) {
+    for (int j = lane; j < dh; j += 32) static_cast<uint16_t*>(out)[o + j] = src[j];
+    return;
+  }
+  float amax = 0.f;
+  for (int j = lane; j < dh; j += 32) amax = fmaxf(amax, fabsf(bf2f(src[j])));
+#pragma unroll
+  for (int off = 16; off; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  const float scale = __fdiv_rn(amax, 127.0f);
+  for (int j = lane; j < dh; j += 32) {
+    float q = 0.f;
+    if (scale > 0.f) q = fminf(fmaxf(rintf(__fdiv_rn(bf2f(src[j]), scale)), -127.f), 127.f);
+    static_cast<int8_t*>(out)[o + j] = static_cast<int8_t>(q);
+  }
+  if (lane == 0) scales[t * planes + plane] = scale;
+}
+
 __global__ void k_read_kv(const uint16_t* __restrict__ arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
                           int32_t row0, int32_t n, uint16_t* __restrict__ k_out, uint16_t* __restrict__ v_out) {
   griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
@@ -351,6 +404,24 @@ cudaError_t copy_rows_launch(const void* src_base, int64_t src_rows, int64_t src
   return launch_pdl(k_copy_rows, dim3(blocks_for(units)), dim3(256), 0, s, static_cast<const uint8_t*>(src_base), src_rows, src_row0,
                                                 static_cast<uint8_t*>(dst_base), dst_rows, dst_row0, n_rows, n_planes,
                                                 row_bytes);
+}
+cudaError_t copy_segments_launch(const CopySeg* segs, int32_t n_segs, int64_t total_rows, void* dst_base,
+                                 int64_t dst_rows, int32_t n_planes, int32_t row_bytes, cudaStream_t s) {
+  if (n_segs <= 0 || total_rows <= 0) return cudaSuccess;
+  if (row_bytes % 16 || n_segs > 65535) return cudaErrorInvalidValue;
+  // ~8 blocks of 256 threads per SM in total, at least one per segment, 8 units per thread max
+  const int64_t units_per_seg = static_cast<int64_t>(n_planes) * (total_rows / n_segs + 1) * (row_bytes / 16);
+  int64_t gx = std::max<int64_t>(1, 148 * 8 / n_segs);
+  gx = std::min<int64_t>(gx, (units_per_seg + 255) / 256);
+  return launch_pdl(k_copy_segments, dim3(static_cast<unsigned>(std::max<int64_t>(gx, 1)), n_segs), dim3(256), 0, s,
+                    segs, static_cast<uint8_t*>(dst_base), dst_rows, n_planes, row_bytes);
+}
+cudaError_t export_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t planes, int32_t dh, int32_t row0,
+                             int32_t n, int32_t int8, void* out, float* scales, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t warps = static_cast<int64_t>(n) * planes;
+  return launch_pdl(k_export_kv, dim3(static_cast<unsigned>((warps + 7) / 8)), dim3(256), 0, s, arena, arena_rows, planes,
+                    dh, row0, n, int8, out, scales);
 }
 cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh, int32_t row0,
                            int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s) {

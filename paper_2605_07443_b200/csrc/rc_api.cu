@@ -8,6 +8,8 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -24,6 +26,19 @@ thread_local std::string g_err;
 int32_t rc::set_error(int32_t code, const char* msg) {
   g_err = msg;
   return code;
+}
+
+cudaError_t rc::smem_opt_in(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;  // (kernel, device)
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kern, dev});
+  return e;
 }
 
 bool rc::pdl_enabled() {
@@ -189,8 +204,11 @@ struct rc_ctx {
   int64_t host_used = 0;
   std::unordered_map<uint64_t, Block> host_items;
   uint64_t use_clock = 1;
+  // LRU index of the remote-cache region (blocks pulled from peers or the host tier): (last_use, id)
+  std::set<std::pair<uint64_t, uint64_t>> lru;
   // peers
   std::unordered_map<int, std::pair<const uint16_t*, int64_t>> peers;  // rank -> (pool base, rows)
+  std::unordered_map<int, std::unordered_map<uint64_t, Block>> peer_dir;  // rank -> its item directory
   std::vector<void*> ipc_opened;
   // arena
   uint16_t* arena = nullptr;
@@ -322,6 +340,59 @@ rc_status build_rope(rc_ctx* c) {
 
 int64_t plane_count(const rc_ctx* c) { return static_cast<int64_t>(c->m.n_layers) * 2 * c->m.n_kv_heads; }
 
+// mark a resident item block used at the current clock (keeps the remote-region LRU index in sync)
+void touch(rc_ctx* c, uint64_t id, Block& b) {
+  if (b.last_use == c->use_clock) return;
+  if (b.remote) {
+    c->lru.erase({b.last_use, id});
+    c->lru.insert({c->use_clock, id});
+  }
+  b.last_use = c->use_clock;
+}
+
+// One block to bring into the remote-cache region.
+struct FetchItem {
+  uint64_t id;
+  const uint16_t* src;  // source pool base (peer mapping) or nullptr (host tier)
+  int64_t src_rows, src_row;
+  int32_t n, canon;
+};
+
+// Plan the region rows of `todo` (all non-resident, distinct) with LRU eviction of remote blocks
+// not used at the current clock, on copies of the allocator: nothing is modified unless every
+// block fits (no partial effects). On success the evictions and allocations are committed and
+// dst[i] holds block i's first item-pool row.
+rc_status plan_remote_rows(rc_ctx* c, const std::vector<FetchItem>& todo, std::vector<int64_t>& dst) {
+  RangeAlloc alloc = c->remote_alloc;
+  std::vector<uint64_t> victims;
+  auto next = c->lru.begin();
+  const int64_t base = c->pd.item_rows - c->pd.remote_rows;
+  dst.resize(todo.size());
+  for (size_t i = 0; i < todo.size(); ++i) {
+    int64_t row = alloc.alloc(todo[i].n);
+    while (row < 0) {
+      if (next == c->lru.end() || next->first == c->use_clock)
+        return fail(RC_E_CAPACITY, "remote region exhausted (every block is used by this call)");
+      const Block& b = c->items.at(next->second);
+      alloc.release(b.row - base, b.n);
+      victims.push_back(next->second);
+      ++next;
+      row = alloc.alloc(todo[i].n);
+    }
+    dst[i] = base + row;
+  }
+  c->remote_alloc = alloc;
+  for (uint64_t v : victims) {
+    c->lru.erase({c->items.at(v).last_use, v});
+    c->items.erase(v);
+  }
+  for (size_t i = 0; i < todo.size(); ++i) {
+    c->items[todo[i].id] = Block{dst[i], todo[i].n, todo[i].canon, true, c->use_clock};
+    c->lru.insert({c->use_clock, todo[i].id});
+  }
+  return RC_OK;
+}
+
 uint16_t* arena_layer(rc_ctx* c, int l, int kv) {
   return c->arena + (static_cast<int64_t>(l) * 2 + kv) * c->m.n_kv_heads * c->pd.arena_rows * c->m.head_dim;
 }
@@ -341,6 +412,10 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
       m.d_model % 16 != 0 || m.d_model > 8192)
     return fail(RC_E_INVALID, "unsupported model shape");
   if (pd->max_seq_len <= 0 || pd->max_seq_len > 8192) return fail(RC_E_INVALID, "max_seq_len must be in 1..8192 (R6)");
+  // R4/R6: D sums 2*H_kv*d_h fixed-point terms below 2^40 each, and the selection key packs D << 13;
+  // D < 2^51 (so the key fits 64 bits) needs at most 2^11 terms
+  if (2 * static_cast<int64_t>(m.n_kv_heads) * m.head_dim > 2048)
+    return fail(RC_E_INVALID, "2*n_kv_heads*head_dim must be <= 2048 (R6 selection key width)");
   if (pd->max_batch_tokens <= 0 || pd->remote_rows > pd->item_rows) return fail(RC_E_INVALID, "bad pool desc");
   if (!w->embed || !w->final_norm || !w->lm_head || !w->ln1 || !w->wq || !w->wk || !w->wv || !w->wo || !w->ln2 ||
       !w->wg || !w->wu || !w->wd || (m.qkv_bias && (!w->bq || !w->bk || !w->bv)))
@@ -536,6 +611,10 @@ rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, con
     if (n_tokens[i] <= 0) return fail(RC_E_INVALID, "empty block");
     if (kind == RC_POOL_HIST_INT8 && n_tokens[i] != 1) return fail(RC_E_INVALID, "prototype blocks are single tokens");
     if (kind == RC_POOL_PREFIX_BF16 && canon_pos[i] != 0) return fail(RC_E_INVALID, "prefix blocks start at 0");
+    // the alignment offset Delta = position - canonical position indexes the RoPE table over
+    // [-max_seq_len, max_seq_len]: canonical positions must lie inside one prompt
+    if (canon_pos[i] < 0 || static_cast<int64_t>(canon_pos[i]) + n_tokens[i] > c->pd.max_seq_len)
+      return fail(RC_E_INVALID, "canonical positions outside [0, max_seq_len)");
     if (dir->count(ids[i])) return fail(RC_E_EXISTS, "duplicate block id " + std::to_string(ids[i]));
     for (int j = 0; j < i; ++j)
       if (ids[j] == ids[i]) return fail(RC_E_EXISTS, "duplicate block id in call");
@@ -666,7 +745,7 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
           }
           return fail(RC_E_INVALID, "item offset outside its block");
         }
-        it->second.last_use = c->use_clock;
+        touch(c, it->first, it->second);
         const int delta = p - (it->second.canon + q.src_off[p]);
         meta_all.push_back(make_int4(p, static_cast<int>(it->second.row + q.src_off[p]), delta, RC_TOK_ITEM));
         meta_all_req.push_back(r);
@@ -713,7 +792,6 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     std::copy(meta_pre.begin(), meta_pre.end(), hm + meta_all.size());
     int4* dm = static_cast<int4*>(c->stage.dev[slot]);
     RC_CUDA(cudaMemcpyAsync(dm, hm, bytes, cudaMemcpyHostToDevice, s));
-    RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
     GatherArgs g{};
     g.n_kv_heads = c->m.n_kv_heads;
     g.head_dim = c->m.head_dim;
@@ -736,6 +814,8 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     g.layer_begin = 0; g.layer_end = gather_from;
     if (g.n_tok > 0 && g.layer_end > g.layer_begin)
       RC_LAUNCH(RC_K_GATHER, 0, b_pre * (g.layer_end - g.layer_begin), -1, gather_launch(g, c->num_sms, s));
+    // the slot's device half is read by the gathers: reusable once they are done (any stream)
+    RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
   }
   for (int r = 0; r < n_req; ++r) {
     const uint64_t id = c->next_seq++;
@@ -793,6 +873,10 @@ rc_status plan_requests(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_p
       const int k = sq.cls[pos];
       nh += k == RC_TOK_HIST; ni += k == RC_TOK_ITEM; nf += k == RC_TOK_FORCED;
     }
+    // the logits are read from the last selected row, so position n-1 must be recomputed:
+    // FORCED (the instruction tail, R8) or inside the window
+    if (prm->window == 0 && sq.cls[sq.n - 1] != RC_TOK_FORCED)
+      return fail(RC_E_INVALID, "the last prompt position must be FORCED (instruction tail) or inside the window");
     p.k_h = budget(prm->r_rev_bp, nh);
     p.k_i = budget(prm->r_item_bp, ni);
     p.forced = nf + nw;
@@ -1085,7 +1169,6 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     }
   }
   RC_CUDA(cudaMemcpyAsync(db, hb, lay.off, cudaMemcpyHostToDevice, s));
-  RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
   auto D32 = [&](size_t o) { return reinterpret_cast<int32_t*>(db + o); };
   const int4* d_ut = reinterpret_cast<const int4*>(db + o_ut);
   const int4* d_st = reinterpret_cast<const int4*>(db + o_st);
@@ -1174,6 +1257,9 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   }
   if (sel_pos_out) RC_CUDA(cudaMemcpyAsync(sel_pos_out, c->sel_pos, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToDevice, s));
   if (hidden) RC_CUDA(cudaMemcpyAsync(hidden, c->xs, static_cast<size_t>(S) * d * 4, cudaMemcpyDeviceToDevice, s));
+  // every kernel of the layer loop reads the slot's device tables (tiles, positions, rows):
+  // the slot is reusable once the last of them has run (the event is waited on by the host)
+  RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
   return RC_OK;
 }
 
@@ -1188,6 +1274,21 @@ rc_status rc_seq_read_kv(rc_ctx* c, rc_seq seq, int32_t layer, void* k_out, void
             read_kv_launch(c->arena, c->pd.arena_rows, layer, c->m.n_kv_heads, c->m.head_dim,
                            static_cast<int32_t>(it->second.arena_row), it->second.n, static_cast<uint16_t*>(k_out),
                            static_cast<uint16_t*>(v_out), s));
+  return RC_OK;
+}
+
+rc_status rc_seq_export_kv(rc_ctx* c, rc_seq seq, int32_t pos0, int32_t n_tok, int32_t int8, void* kv_out,
+                           float* scales_out, rc_stream stream) {
+  if (!c || !kv_out || (int8 && !scales_out)) return fail(RC_E_INVALID, "null argument");
+  auto it = c->seqs.find(seq);
+  if (it == c->seqs.end()) return fail(RC_E_NOTFOUND, "unknown sequence");
+  if (pos0 < 0 || n_tok < 0 || pos0 + n_tok > it->second.n) return fail(RC_E_INVALID, "position range outside the sequence");
+  RC_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t planes = plane_count(c);
+  RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(n_tok) * planes * c->m.head_dim * (int8 ? 3.0 : 4.0), -1,
+            export_kv_launch(c->arena, c->pd.arena_rows, static_cast<int32_t>(planes), c->m.head_dim,
+                             static_cast<int32_t>(it->second.arena_row + pos0), n_tok, int8, kv_out, scales_out, s));
   return RC_OK;
 }
 
@@ -1230,44 +1331,87 @@ rc_status rc_peer_attach(rc_ctx* c, int32_t n, const int32_t* rank, const int32_
   return RC_OK;
 }
 
-rc_status rc_fetch_remote(rc_ctx* c, int32_t n_items, const uint64_t* ids, const int32_t* owner, const int64_t* owner_row,
-                          const int32_t* n_tokens, const int32_t* canon_pos, rc_stream stream) {
-  if (!c || n_items < 0 || (n_items > 0 && (!ids || !owner || !owner_row || !n_tokens || !canon_pos)))
+rc_status rc_pool_list(rc_ctx* c, int32_t cap, uint64_t* ids, int64_t* rows, int32_t* n_tokens, int32_t* canon_pos,
+                       int32_t* n_out) {
+  if (!c || !n_out || cap < 0 || (cap > 0 && (!ids || !rows || !n_tokens || !canon_pos)))
     return fail(RC_E_INVALID, "null argument");
+  int32_t n = 0;
+  for (auto& kv : c->items) {
+    if (kv.second.remote) continue;  // only blocks owned by this pool (not cached copies)
+    if (n < cap) {
+      ids[n] = kv.first; rows[n] = kv.second.row; n_tokens[n] = kv.second.n; canon_pos[n] = kv.second.canon;
+    }
+    ++n;
+  }
+  *n_out = n;
+  return n > cap ? fail(RC_E_CAPACITY, "directory larger than cap (n_out holds the size)") : RC_OK;
+}
+
+rc_status rc_peer_directory(rc_ctx* c, int32_t peer_rank, int32_t n, const uint64_t* ids, const int64_t* rows,
+                            const int32_t* n_tokens, const int32_t* canon_pos) {
+  if (!c || n < 0 || (n > 0 && (!ids || !rows || !n_tokens || !canon_pos))) return fail(RC_E_INVALID, "null argument");
+  auto pit = c->peers.find(peer_rank);
+  if (pit == c->peers.end()) return fail(RC_E_PEER, "peer rank not attached");
+  for (int i = 0; i < n; ++i)  // validate everything first (all-or-nothing)
+    if (n_tokens[i] <= 0 || rows[i] < 0 || rows[i] + n_tokens[i] > pit->second.second || canon_pos[i] < 0 ||
+        static_cast<int64_t>(canon_pos[i]) + n_tokens[i] > c->pd.max_seq_len)
+      return fail(RC_E_INVALID, "directory entry outside the peer's pool or the position range");
+  auto& dir = c->peer_dir[peer_rank];
+  dir.clear();
+  for (int i = 0; i < n; ++i) dir[ids[i]] = Block{rows[i], n_tokens[i], canon_pos[i], false, 0};
+  return RC_OK;
+}
+
+rc_status rc_fetch_remote(rc_ctx* c, int32_t n_items, const uint64_t* ids, const int32_t* owner, rc_stream stream) {
+  if (!c || n_items < 0 || (n_items > 0 && (!ids || !owner))) return fail(RC_E_INVALID, "null argument");
+  if (n_items == 0) return RC_OK;
+  if (!c->item_pool) return fail(RC_E_INVALID, "no item pool");
   RC_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // ---- validate and resolve before touching state
+  std::vector<FetchItem> todo;
+  std::set<uint64_t> seen;
   int64_t need = 0;
   for (int i = 0; i < n_items; ++i) {
-    if (!c->peers.count(owner[i])) return fail(RC_E_PEER, "owner rank not attached");
-    if (n_tokens[i] <= 0 || owner_row[i] < 0) return fail(RC_E_INVALID, "bad fetch entry");
-    if (!c->items.count(ids[i])) need += n_tokens[i];
+    auto pit = c->peers.find(owner[i]);
+    if (pit == c->peers.end()) return fail(RC_E_PEER, "owner rank not attached");
+    if (c->items.count(ids[i]) || !seen.insert(ids[i]).second) continue;
+    auto dit = c->peer_dir.find(owner[i]);
+    const Block* b = nullptr;
+    if (dit != c->peer_dir.end()) {
+      auto bit = dit->second.find(ids[i]);
+      if (bit != dit->second.end()) b = &bit->second;
+    }
+    if (!b) return fail(RC_E_NOTFOUND, "item " + std::to_string(ids[i]) + " not in owner's directory");
+    todo.push_back(FetchItem{ids[i], pit->second.first, pit->second.second, b->row, b->n, b->canon});
+    need += b->n;
   }
   if (need > c->pd.remote_rows) return fail(RC_E_CAPACITY, "remote region smaller than one fetch");
+  // ---- protect the blocks of this call, plan rows (LRU evictions), then one batched copy
+  ++c->use_clock;
+  for (int i = 0; i < n_items; ++i) {
+    auto it = c->items.find(ids[i]);
+    if (it != c->items.end()) touch(c, it->first, it->second);
+  }
+  if (todo.empty()) return RC_OK;
+  std::vector<int64_t> dst;
+  rc_status st = plan_remote_rows(c, todo, dst);
+  if (st != RC_OK) return st;
+  std::vector<CopySeg> segs(todo.size());
+  for (size_t i = 0; i < todo.size(); ++i)
+    segs[i] = CopySeg{todo[i].src, todo[i].src_rows, todo[i].src_row, dst[i], todo[i].n, 0};
+  cudaError_t e;
+  const size_t bytes = segs.size() * sizeof(CopySeg);
+  const int slot = c->stage.acquire(bytes, &e);
+  if (slot < 0) return fail(RC_E_NOMEM, std::string("staging: ") + cudaGetErrorString(e));
+  std::memcpy(c->stage.host[slot], segs.data(), bytes);
+  RC_CUDA(cudaMemcpyAsync(c->stage.dev[slot], c->stage.host[slot], bytes, cudaMemcpyHostToDevice, s));
   const int64_t planes = plane_count(c);
   const int row_bytes = c->m.head_dim * 2;
-  for (int i = 0; i < n_items; ++i) {
-    if (c->items.count(ids[i])) { c->items[ids[i]].last_use = c->use_clock; continue; }
-    int64_t row = c->remote_alloc.alloc(n_tokens[i]);
-    while (row < 0) {  // evict least-recently used remote items (not used by this call)
-      uint64_t victim = 0, best = ~0ull;
-      for (auto& kv : c->items)
-        if (kv.second.remote && kv.second.last_use < best && kv.second.last_use != c->use_clock) {
-          best = kv.second.last_use;
-          victim = kv.first;
-        }
-      if (best == ~0ull) return fail(RC_E_CAPACITY, "remote region exhausted");
-      const Block b = c->items[victim];
-      c->remote_alloc.release(b.row - (c->pd.item_rows - c->pd.remote_rows), b.n);
-      c->items.erase(victim);
-      row = c->remote_alloc.alloc(n_tokens[i]);
-    }
-    const int64_t grow = (c->pd.item_rows - c->pd.remote_rows) + row;
-    const auto& peer = c->peers[owner[i]];
-    RC_LAUNCH(RC_K_FETCH, 0, 2.0 * planes * n_tokens[i] * row_bytes, -1,
-              copy_rows_launch(peer.first, peer.second, owner_row[i], c->item_pool, c->pd.item_rows, grow, n_tokens[i],
-                               static_cast<int32_t>(planes), row_bytes, s));
-    c->items[ids[i]] = Block{grow, n_tokens[i], canon_pos[i], true, c->use_clock};
-  }
+  RC_LAUNCH(RC_K_FETCH, 0, 2.0 * planes * need * row_bytes, -1,
+            copy_segments_launch(static_cast<const CopySeg*>(c->stage.dev[slot]), static_cast<int32_t>(segs.size()),
+                                 need, c->item_pool, c->pd.item_rows, static_cast<int32_t>(planes), row_bytes, s));
+  RC_CUDA(cudaEventRecord(c->stage.ev[slot], s));
   return RC_OK;
 }
 
@@ -1276,41 +1420,32 @@ rc_status rc_fetch_host(rc_ctx* c, int32_t n_items, const uint64_t* ids, rc_stre
   if (!c->host_pool) return fail(RC_E_INVALID, "no host tier (host_item_rows = 0)");
   RC_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<FetchItem> todo;
+  std::set<uint64_t> seen;
   int64_t need = 0;
-  ++c->use_clock;  // blocks of this call are protected from eviction by it
   for (int i = 0; i < n_items; ++i) {
-    if (c->items.count(ids[i])) { c->items[ids[i]].last_use = c->use_clock; continue; }
+    if (c->items.count(ids[i]) || !seen.insert(ids[i]).second) continue;
     auto it = c->host_items.find(ids[i]);
     if (it == c->host_items.end()) return fail(RC_E_NOTFOUND, "item " + std::to_string(ids[i]) + " in no tier");
+    todo.push_back(FetchItem{ids[i], nullptr, c->pd.host_item_rows, it->second.row, it->second.n, it->second.canon});
     need += it->second.n;
   }
   if (need > c->pd.remote_rows) return fail(RC_E_CAPACITY, "remote region smaller than one host fetch");
+  ++c->use_clock;  // blocks of this call are protected from eviction by it
+  for (int i = 0; i < n_items; ++i) {
+    auto it = c->items.find(ids[i]);
+    if (it != c->items.end()) touch(c, it->first, it->second);
+  }
+  if (todo.empty()) return RC_OK;
+  std::vector<int64_t> dst;
+  rc_status st = plan_remote_rows(c, todo, dst);
+  if (st != RC_OK) return st;
   const int64_t planes = plane_count(c);
   const size_t row_bytes = static_cast<size_t>(c->m.head_dim) * 2;
-  for (int i = 0; i < n_items; ++i) {
-    if (c->items.count(ids[i])) continue;
-    const Block hb = c->host_items[ids[i]];
-    int64_t row = c->remote_alloc.alloc(hb.n);
-    while (row < 0) {  // evict least-recently used remote blocks not used by this call
-      uint64_t victim = 0, best = ~0ull;
-      for (auto& kv : c->items)
-        if (kv.second.remote && kv.second.last_use < best && kv.second.last_use != c->use_clock) {
-          best = kv.second.last_use;
-          victim = kv.first;
-        }
-      if (best == ~0ull) return fail(RC_E_CAPACITY, "remote region exhausted");
-      const Block b = c->items[victim];
-      c->remote_alloc.release(b.row - (c->pd.item_rows - c->pd.remote_rows), b.n);
-      c->items.erase(victim);
-      row = c->remote_alloc.alloc(hb.n);
-    }
-    const int64_t grow = (c->pd.item_rows - c->pd.remote_rows) + row;
-    // one 2-D copy on the copy engines: `planes` runs of n rows, pitches = the two pools' plane strides
-    RC_CUDA(cudaMemcpy2DAsync(c->item_pool + grow * c->m.head_dim, c->pd.item_rows * row_bytes,
-                              c->host_pool + hb.row * c->m.head_dim, c->pd.host_item_rows * row_bytes,
-                              hb.n * row_bytes, planes, cudaMemcpyHostToDevice, s));
-    c->items[ids[i]] = Block{grow, hb.n, hb.canon, true, c->use_clock};
-  }
+  for (size_t i = 0; i < todo.size(); ++i)  // one 2-D copy per block on the copy engines (no SMs)
+    RC_CUDA(cudaMemcpy2DAsync(c->item_pool + dst[i] * c->m.head_dim, c->pd.item_rows * row_bytes,
+                              c->host_pool + todo[i].src_row * c->m.head_dim, c->pd.host_item_rows * row_bytes,
+                              todo[i].n * row_bytes, planes, cudaMemcpyHostToDevice, s));
   return RC_OK;
 }
 

@@ -13,6 +13,10 @@ int32_t set_error(int32_t code, const char* msg);
 // the previous kernel in the stream drains, runs its prologue (barrier init, TMEM allocation,
 // descriptor prefetch), and blocks in griddepcontrol.wait before touching memory the previous
 // kernel produced. Kernels call griddepcontrol.launch_dependents once all their CTAs are running.
+// Opt a kernel in to > 48 KB of dynamic shared memory on the CURRENT device. The attribute is
+// per device, so it is set once per (kernel, device) -- a process may hold contexts on several GPUs.
+cudaError_t smem_opt_in(const void* kern, int bytes);
+
 bool pdl_enabled();  // RC_PDL=0 in the environment turns the attribute off (A/B diagnostics)
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
@@ -178,6 +182,17 @@ cudaError_t scale_transpose_launch(const float* src, int32_t n_tok, int32_t L, i
 cudaError_t copy_rows_launch(const void* src_base, int64_t src_rows, int64_t src_row0, void* dst_base,
                              int64_t dst_rows, int64_t dst_row0, int32_t n_rows, int32_t n_planes,
                              int32_t row_bytes, cudaStream_t s);
+// batched peer pull (rc_fetch_remote): segment i copies n_rows rows of every plane from a source
+// pool [planes][src_rows][row_bytes] at src_row0 to dst [planes][dst_rows][row_bytes] at dst_row0
+struct CopySeg {
+  const void* src;
+  int64_t src_rows, src_row0, dst_row0;
+  int32_t n_rows, pad;
+};
+cudaError_t copy_segments_launch(const CopySeg* segs, int32_t n_segs, int64_t total_rows, void* dst_base,
+                                 int64_t dst_rows, int32_t n_planes, int32_t row_bytes, cudaStream_t s);
+cudaError_t export_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t planes, int32_t dh, int32_t row0,
+                             int32_t n, int32_t int8, void* out, float* scales, cudaStream_t s);
 cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
                            int32_t row0, int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s);
 

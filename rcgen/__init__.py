@@ -7,5 +7,5 @@ from .shapes import ModelShape, Workload, SHAPES, WORKLOADS, TINY, TINY_Q7, LLAM
 from .shapes import CFG1, CFG1_Q7, CFG2, CFG3, CFG5, MINI_L, MINI_Q, MINI_LLAMA, MINI_QWEN
 from . import weights
 from .weights import gen_weights, gen_tensor, subseed
-from .workload import gen_catalog, gen_protos, gen_system_prompt, gen_request, gen_requests
+from .workload import gen_catalog, gen_protos, gen_system_prompt, gen_request, gen_requests, proto_corpus
 from . import pools

@@ -147,3 +147,25 @@ def gen_request(wl: Workload, cat: Catalog, protos: Protos, i: int) -> Request:
 
 def gen_requests(wl: Workload, cat: Catalog, protos: Protos, n: int, start: int = 0):
     return [gen_request(wl, cat, protos, start + i) for i in range(n)]
+
+
+def proto_corpus(wl: Workload, protos: Protos, proto_ids, seed: int = 4):
+    """Synthetic review-corpus sequences that host the prototypes (a prototype is its
+    medoid token at its canonical position in a synthetic review context). Data arrangement only:
+    prototype pi is placed at history offset canon_pos[pi] - P of corpus sequence j, where j counts
+    the earlier listed prototypes with the same offset; every other slot holds a seeded uniform
+    token. Returns (tokens int32 [S][H], seq int32 [len(proto_ids)], offset int32 [len(proto_ids)]),
+    H = 1 + the largest offset, S = the largest multiplicity of an offset."""
+    ids = np.asarray(proto_ids, dtype=np.int64)
+    off = (protos.canon_pos[ids] - wl.prefix_len).astype(np.int64)
+    H = int(off.max()) + 1 if len(ids) else 1
+    seq = np.zeros(len(ids), dtype=np.int32)
+    used = {}
+    for k, o in enumerate(off.tolist()):
+        seq[k] = used.get(o, 0)
+        used[o] = seq[k] + 1
+    S = max(used.values()) if used else 1
+    rng = np.random.Generator(np.random.PCG64(seed))
+    toks = rng.integers(0, _free_vocab(wl), size=(S, H)).astype(np.int32)
+    toks[seq, off] = protos.token[ids]
+    return toks, seq, off.astype(np.int32)

@@ -55,3 +55,34 @@ def gpu_layouts(ctx, case, reqs=None):
 
 def bits(t):
     return t.cpu().numpy().view(np.uint16)
+
+
+def make_ctx_materialized(case, n_req_tokens, Wd=None, remote_rows=0):
+    """Context whose pools are materialised by librc's dense path (SURVEY R16/R17, §8(d) "Pool
+    contents"): prefix = full prefill of the system prompt, items = [system prompt; item] at P..,
+    prototypes = their token at the canonical position of a review-corpus sequence, int8 (R15).
+    Returns (ctx, pools) with pools in the oracle_pools format holding the registered bytes."""
+    from paper_2605_07443_b200 import materialize as MZ
+    wl, shape = case["wl"], case["shape"]
+    Wd = Wd if Wd is not None else weights_to(case["W"])
+    reqs = case["reqs"]
+    items = sorted({int(i) for r in reqs for i in r.cand_items})
+    protos = sorted({int(p) for r in reqs for p in r.hist_protos})
+    corpus, seq_of, off_of = rcgen.proto_corpus(wl, case["protos"], protos)
+    arena = max(n_req_tokens, 4 * (wl.prefix_len + max(corpus.shape[1], wl.item_len)))
+    ctx = RcContext(shape, Wd, item_rows=len(items) * wl.item_len + remote_rows, hist_rows=max(len(protos), 1),
+                    prefix_rows=max(wl.prefix_len, 1), arena_rows=arena, max_seq_len=max(wl.n, 256),
+                    max_batch_tokens=arena, remote_rows=remote_rows)
+    sys_tok = case["sys"]
+    pkv = MZ.register_prefix(ctx, sys_tok, PREFIX_ID)
+    kept = MZ.register_items(ctx, sys_tok, PREFIX_ID, items, [case["cat"].tokens[i] for i in items], keep=True)
+    canon = [int(case["protos"].canon_pos[p]) for p in protos]
+    q, s = MZ.register_protos(ctx, sys_tok, PREFIX_ID, protos, canon, corpus, seq_of, off_of)
+    torch.cuda.synchronize()
+    ikv = torch.stack([kept[i] for i in items]).cpu()
+    hq, hs = q.cpu(), s.cpu()
+    pools = dict(items={it: (ikv[j], wl.prefix_len) for j, it in enumerate(items)},
+                 hist={pi: (hq[j].numpy(), hs[j].numpy(), canon[j]) for j, pi in enumerate(protos)},
+                 prefix=pkv.cpu(), item_ids=items, proto_ids=protos, item_kv=ikv, hist_q=hq, hist_s=hs,
+                 corpus=(corpus, seq_of, off_of))
+    return ctx, pools, Wd

@@ -31,7 +31,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 TOL = 1e-2
 R_BP = 1500
 C = 1
-LOGITS_TOL_PER_REQUEST = 1.25e-2
+LOGITS_TOL_PER_REQUEST = 1e-2   # north_star: rel-L2 <= 1e-2 on logits, per request
 _LOGITS = {}
 CHECK_REQS = tuple(int(x) for x in os.environ.get("RC_FULLSIZE_REQS", "0,31").split(","))
 
@@ -72,6 +72,12 @@ def _setup(wl, batch, check_reqs):
     res["kv_last"] = {r: tuple(t.cpu().numpy().view(np.uint16) for t in ctx.read_kv(seqs[r], shape.n_layers - 1, n))
                       for r in check_reqs}
     cand_off = np.concatenate([[0], np.cumsum([len(l["cand_idtok"]) for l in lays])])
+    ctx.release(seqs)
+    # run-to-run determinism: the same batch assembled and prefilled again
+    seqs = ctx.assemble(lays, prefix_id=1, gather_from=C)
+    out2 = ctx.selective_prefill(seqs, R_BP, R_BP, check_layer=C, hidden=True, n_cand=n_cand)
+    torch.cuda.synchronize()
+    res["rerun"] = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out2.items()}
     ctx.release(seqs)
     ctx.close()
     Wh = {"embed": W["embed"].cpu(), "norm": W["norm"].cpu(), "lm_head": W["lm_head"].cpu(),
@@ -122,7 +128,7 @@ def test_cfg3_batch32_request_matches_oracle(run, r):
            "K_last": rel_l2(Kg, forced["K"][L - 1][sel]), "V_last": rel_l2(Vg, forced["V"][L - 1][sel])}
     print("fullsize parity", json.dumps(err))
     _LOGITS[r] = (res["logits"][r], forced["logits"])
-    assert jac >= 0.8, err
+    assert jac >= 0.95, err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["V_last"] < TOL, err
     # DESIGN.md R-TOL: per request the last-token logits sit at the bf16 floor of this 32-layer model
     # (0.90-1.02% measured; tests/test_gpu_accuracy_probe.py: torch bf16 with an fp32 residual 0.94%,
@@ -133,9 +139,22 @@ def test_cfg3_batch32_request_matches_oracle(run, r):
     assert len(keep) > 0 and np.array_equal(res["kv_last"][r][0][keep], K_asm[L - 1][keep])
     cs = res["cand_scores"][d["cand_off"][r]:d["cand_off"][r + 1]]
     ref = forced["cand_scores"]
-    assert np.allclose(cs, ref, rtol=0.05, atol=0.05 * np.abs(ref).max())
+    assert np.array_equal(cs, res["logits"][r][lay.cand_idtok])       # the readout itself is exact
+    # each candidate score is a logit: within 5x the per-element RMS that rel-L2 <= 1e-2 allows
+    assert np.max(np.abs(cs - ref)) <= 5 * TOL * np.sqrt(np.mean(forced["logits"] ** 2))
     print("fullsize ranking: resolvable top-10 positions checked",
           assert_top10_ranking(cs, ref, rms_err(res["logits"][r], forced["logits"])))
+
+
+def test_cfg3_batch32_rerun_is_deterministic(run):
+    """The same batch twice (re-assembled): identical selection, logits and hidden states bit for bit."""
+    res, _ = run
+    rr = res["rerun"]
+    assert np.array_equal(rr["sel_pos"], res["sel_pos"])
+    same = {k: bool(np.array_equal(rr[k], res[k])) for k in ("logits", "hidden", "cand_scores")}
+    diff = {k: float(np.max(np.abs(rr[k] - res[k]))) for k in ("logits", "hidden")}
+    print("rerun bitwise identical", json.dumps(same), "max |diff|", json.dumps(diff))
+    assert all(same.values()), (same, diff)
 
 
 def test_cfg3_batch32_logits_over_checked_set():
@@ -165,7 +184,7 @@ def test_cfg5_qwen2_8k_batch4_request_matches_oracle():
            "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
            "K_last": rel_l2(Kg, forced["K"][L - 1][sel])}
     print("fullsize cfg5 parity", json.dumps(err))
-    assert jac >= 0.8, err
+    assert jac >= 0.95, err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
 
 
@@ -187,5 +206,5 @@ def test_batch1_request_matches_oracle(wl):
            "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
            "K_last": rel_l2(Kg, forced["K"][L - 1][sel])}
     print(f"fullsize {wl.name} batch-1 parity", json.dumps(err))
-    assert jac >= 0.8, err
+    assert jac >= 0.95, err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err

@@ -142,6 +142,22 @@ def test_deviation_and_selection_bitexact(n_u, width, r_bp, window):
 
 
 # ----------------------------------------------------------------------------- end to end
+def _near_tie_swaps(sel, own, lay):
+    """R21 on small prompts (|Sel| ~ 28, where one swap already puts the Jaccard under 0.95): at most
+    one swapped pair per class, and it is a near-tie of the oracle's own scores (within 2 %)."""
+    a, b = set(int(x) for x in sel), set(int(x) for x in own["sel"])
+    S = own["S"].astype(np.float64)
+    for cl in (HIST, ITEM):
+        gin = [p for p in a - b if lay.cls[p] == cl]
+        gout = [p for p in b - a if lay.cls[p] == cl]
+        if len(gin) != len(gout) or len(gin) > 1:
+            return False
+        if any(abs(S[p] - S[q]) > 0.02 * max(S[p], S[q]) for p, q in zip(gin, gout)):
+            return False
+    return True
+
+
+
 def _run_gpu(wl, case, pools, r_bp, c=1, forced=None, no_prefix=False, hidden=True, window=0, attn_kernel=0):
     G = _gpu()
     n_tok = sum(l.n for l in layouts(case))
@@ -201,7 +217,7 @@ def test_selective_prefill_parity(wl, r_bp, c):
     # selection: same budgets; Jaccard vs the oracle's own choice (bf16 noise may flip near-ties)
     assert len(own["sel"]) == len(sel)
     jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
-    assert jac >= 0.8, jac
+    assert jac >= 0.95 or _near_tie_swaps(sel, own, lay), jac
     assert rel_l2(res["logits"][0], forced["logits"]) < TOL
     assert rel_l2(res["hidden"], forced["x_sel"]) < TOL
     L = case["shape"].n_layers
@@ -213,7 +229,8 @@ def test_selective_prefill_parity(wl, r_bp, c):
     keep = np.array([p for p in range(lay.n) if p not in set(sel.tolist()) and dfn[L - 1, p]])
     if len(keep):
         assert np.array_equal(res["kv_last"][0][0][keep], K_asm[L - 1][keep])
-    assert np.allclose(res["cand_scores"], forced["cand_scores"], rtol=0.05, atol=0.05 * np.abs(forced["cand_scores"]).max())
+    assert np.array_equal(res["cand_scores"], res["logits"][0][lay.cand_idtok])   # the readout itself is exact
+    assert np.max(np.abs(res["cand_scores"] - forced["cand_scores"])) <= 5 * TOL * np.sqrt(np.mean(forced["logits"] ** 2))
     assert_top10_ranking(res["cand_scores"], forced["cand_scores"], rms_err(res["logits"][0], forced["logits"]))
 
 
@@ -262,7 +279,7 @@ def test_item_miss_recomputed_matches_oracle():
     forced, own = _oracle_forced(case, pools, lay_m, sel, 1500)
     assert len(own["sel"]) == len(sel)
     jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
-    assert jac >= 0.8, jac
+    assert jac >= 0.95 or _near_tie_swaps(sel, own, lay), jac
     assert rel_l2(res["logits"][0], forced["logits"]) < TOL
     assert rel_l2(res["hidden"], forced["x_sel"]) < TOL
 
@@ -296,7 +313,7 @@ def test_attention_launch_shapes_match_oracle(wl, attn_kernel):
         sel = res["sel_pos"][off[r]:off[r + 1]]
         forced, own = _oracle_forced(case, pools, lay, sel, 1500)
         jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
-        assert jac >= 0.8, jac
+        assert jac >= 0.95 or _near_tie_swaps(sel, own, lay), jac
         assert rel_l2(res["logits"][r], forced["logits"]) < TOL
         assert rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
 
@@ -393,9 +410,17 @@ def test_attention_mass_scores_and_selection(wl, c, lam):
         own = selective_prefill(m, lay, K, V, 1500, 1500, check_layer=c, lam=lam)
         forced = selective_prefill(m, lay, K, V, 1500, 1500, check_layer=c, lam=lam, forced_sel=sel)
         reuse = np.isin(lay.cls, [HIST, ITEM])
-        assert rel_l2(S_gpu[reuse].astype(np.float64), own["S"][reuse].astype(np.float64)) < 2e-2
+        # element by element: S = rint((1 - lambda) A + lambda D) of every HIST/ITEM row. A sums
+        # softmax probabilities of bf16 Q/K scores (relative error ~ |s| 2^-8 per score, R2-FX) and D
+        # the fixed-point |K_new - K_st| of bf16 operands; bound: 5 % of the row's own score plus
+        # 0.5 % of the largest score (rows whose mass is tiny carry only absolute error)
+        Sg, So = S_gpu[reuse].astype(np.float64), own["S"][reuse].astype(np.float64)
+        err = np.abs(Sg - So)
+        print(f"NEXT-1 S per element: max rel {np.max(err / np.maximum(So, 1)):.3e}, "
+              f"max abs / max S {err.max() / So.max():.3e}")
+        assert np.all(err <= 0.05 * So + 5e-3 * So.max()), (err / np.maximum(So, 1)).max()
         jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
-        assert jac >= 0.8, jac
+        assert jac >= 0.95 or _near_tie_swaps(sel, own, lay), jac
         assert rel_l2(res["logits"][r], forced["logits"]) < TOL
         assert rel_l2(res["hidden"][res["sel_off"][r]:res["sel_off"][r + 1]], forced["x_sel"]) < TOL
 
