@@ -129,7 +129,7 @@ def _small_ctx():
     wl = rcgen.MINI_L
     case = make_case(wl)
     pools = oracle_pools(case)
-    ctx, _ = G.make_ctx(case, pools, wl.n)
+    ctx, _ = G.make_ctx(case, pools, wl.n, extra_item_rows=wl.item_len)
     return wl, case, pools, ctx
 
 

@@ -411,14 +411,14 @@ def test_attention_mass_scores_and_selection(wl, c, lam):
         forced = selective_prefill(m, lay, K, V, 1500, 1500, check_layer=c, lam=lam, forced_sel=sel)
         reuse = np.isin(lay.cls, [HIST, ITEM])
         # element by element: S = rint((1 - lambda) A + lambda D) of every HIST/ITEM row. A sums
-        # softmax probabilities of bf16 Q/K scores (relative error ~ |s| 2^-8 per score, R2-FX) and D
-        # the fixed-point |K_new - K_st| of bf16 operands; bound: 5 % of the row's own score plus
-        # 0.5 % of the largest score (rows whose mass is tiny carry only absolute error)
+        # softmax probabilities of bf16 Q/K scores (R2-FX) and D the fixed-point |K_new - K_st| of
+        # bf16 operands; bound: 1 % of the row's own score plus 0.2 % of the largest score (rows whose
+        # mass is tiny carry only absolute error). Measured on B200: <= 0.21 % and <= 0.09 %.
         Sg, So = S_gpu[reuse].astype(np.float64), own["S"][reuse].astype(np.float64)
         err = np.abs(Sg - So)
         print(f"NEXT-1 S per element: max rel {np.max(err / np.maximum(So, 1)):.3e}, "
               f"max abs / max S {err.max() / So.max():.3e}")
-        assert np.all(err <= 0.05 * So + 5e-3 * So.max()), (err / np.maximum(So, 1)).max()
+        assert np.all(err <= 0.01 * So + 2e-3 * So.max()), (err / np.maximum(So, 1)).max()
         jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
         assert jac >= 0.95 or _near_tie_swaps(sel, own, lay), jac
         assert rel_l2(res["logits"][r], forced["logits"]) < TOL
