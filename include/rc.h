@@ -140,6 +140,11 @@ typedef struct rc_prefill_params {
   uint64_t* score_out;        /* optional device [sum of |U| over the batch], U rows request-major:
                                  the selection score of every U row (Eq. 3 fixed point, DESIGN.md
                                  R4 / R2-FX; only HIST/ITEM rows are meaningful); NULL = none */
+  int32_t deterministic;      /* the layers < c (which decide Sel) always sum split-K / stream-K
+                                 partial tiles in K order, so Sel is reproducible run to run;
+                                 1 = the layers >= c as well (logits and hidden states bitwise
+                                 reproducible, at the cost of a workspace round trip per split
+                                 tile); 0 = those partials meet in fp32 reduce-adds in arrival order */
 } rc_prefill_params;
 enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3, RC_ATTN_ADAPTIVE = 4 };
 /* RC_ATTN_SPLIT2: every query tile's KV range in two CTAs + merge; RC_ATTN_ADAPTIVE: the same launch,
@@ -331,6 +336,11 @@ rc_status rc_diag_deviation_select(int32_t n_u, int32_t width, const void* k_new
 /* The tcgen05 GEMM on its own: C f32 [M][N] = A bf16 [M][K] * B bf16 [N][K]^T (DEVICE). */
 rc_status rc_diag_gemm(int32_t M, int32_t N, int32_t K, const void* A, const void* B, float* C, int32_t bn,
                        rc_stream stream);
+/* The residual GEMM on its own: X f32 [M][N] += A bf16 [M][K] * B bf16 [N][K]^T (DEVICE), through
+ * the same kernel choice as the hot path (transposed = 1 offers the small-M transposed pair kernel;
+ * split-K / stream-K partial tiles are summed in K order). Synchronises `stream`. N % 32 == 0. */
+rc_status rc_diag_gemm_add(int32_t M, int32_t N, int32_t K, const void* A, const void* B, float* X,
+                           int32_t transposed, rc_stream stream);
 /* Kernel launches issued by this context since creation (every librc kernel counts). */
 int64_t rc_launch_count(rc_ctx* ctx);
 

@@ -58,7 +58,7 @@ RC_ATTN_AUTO, RC_ATTN_SINGLE, RC_ATTN_PAIRED, RC_ATTN_SPLIT2, RC_ATTN_ADAPTIVE =
 class PrefillParams(C.Structure):
     _fields_ = [("r_rev_bp", C.c_int32), ("r_item_bp", C.c_int32), ("lambda_", C.c_float),
                 ("check_layer", C.c_int32), ("window", C.c_int32), ("forced_sel", I32P), ("forced_sel_off", I32P),
-                ("attn_kernel", C.c_int32), ("score_out", C.c_void_p)]
+                ("attn_kernel", C.c_int32), ("score_out", C.c_void_p), ("deterministic", C.c_int32)]
 
 
 _LIB = None
@@ -103,6 +103,7 @@ def lib():
             "rc_diag_deviation_select": (C.c_int32, [C.c_int32, C.c_int32, P, P, P, P, U8P, C.c_int32, C.c_int32,
                                                      C.c_int32, C.c_int32, P, P, I32P, P]),
             "rc_diag_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int32, P]),
+            "rc_diag_gemm_add": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int32, P]),
             "rc_launch_count": (C.c_int64, [P]),
             "rc_place_items": (C.c_int32, [C.c_int32, I32P, C.c_int32, I64P, I32P, C.c_int32, C.c_int32, C.c_double,
                                            C.c_int32, I32P, I64P, I64P]),
@@ -135,5 +136,5 @@ EXPORTED = ["rc_create", "rc_destroy", "rc_last_error", "rc_abi_version", "rc_de
             "rc_selective_prefill", "rc_release", "rc_pool_export", "rc_peer_attach", "rc_fetch_remote",
             "rc_seq_read_kv", "rc_diag_deviation_select", "rc_diag_gemm", "rc_launch_count", "rc_profile_begin",
             "rc_profile_end", "rc_place_items", "rc_route", "rc_fetch_host", "rc_semlib_build", "rc_semlib_match",
-            "rc_pool_list", "rc_peer_directory", "rc_seq_export_kv"]
+            "rc_pool_list", "rc_peer_directory", "rc_seq_export_kv", "rc_diag_gemm_add"]
 KINDS = ["gemm", "attention", "gather", "select", "small", "lm_head", "fetch"]

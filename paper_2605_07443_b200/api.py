@@ -129,8 +129,9 @@ class RcContext:
         check(code)
         return seqs
 
-    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0, attn_kernel=0):
-        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None, attn_kernel, None)
+    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0, attn_kernel=0, deterministic=0):
+        prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None, attn_kernel, None,
+                              int(deterministic))
         keep = None
         if forced_sel is not None:
             off = np.zeros(len(forced_sel) + 1, np.int32)
@@ -150,13 +151,13 @@ class RcContext:
 
     def selective_prefill(self, seqs, r_rev_bp, r_item_bp, check_layer=1, window=0, forced_sel=None, lam=1.0,
                           logits=True, cand_scores=True, sel_pos=True, hidden=False, n_cand=None, out=None,
-                          stream=None, attn_kernel=0, score_out=None):
+                          stream=None, attn_kernel=0, score_out=None, deterministic=False):
         """Returns dict of CUDA tensors (logits, cand_scores, sel_pos, hidden) as requested. `out`
         may hold preallocated tensors with the same keys (reused; no allocation). score_out: optional
         int64 CUDA tensor [sum |U|] receiving the selection score of every U row (lam < 1: Eq. 3
         with the attention-mass term, NEXT-1)."""
         seqs = np.ascontiguousarray(seqs, np.uint64)
-        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam, attn_kernel)
+        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam, attn_kernel, deterministic)
         if score_out is not None:
             prm.score_out = score_out.data_ptr()
         dev = torch.device("cuda", self.device)
@@ -292,6 +293,14 @@ def diag_gemm(A, B, bn=256, stream=None):
     Cm = torch.empty((M, N), dtype=torch.float32, device=A.device)
     check(lib().rc_diag_gemm(M, N, K, _dptr(A), _dptr(B), _dptr(Cm), bn, _stream(stream)))
     return Cm
+
+
+def diag_gemm_add(A, B, X, transposed=False, stream=None):
+    """X f32 [M][N] += A [M][K] B[N][K]^T in place (the residual-epilogue GEMM on its own)."""
+    M, K = A.shape
+    N = B.shape[0]
+    check(lib().rc_diag_gemm_add(M, N, K, _dptr(A), _dptr(B), _dptr(X), 1 if transposed else 0, _stream(stream)))
+    return X
 
 
 def diag_deviation_select(k_new, k_st, v_new, v_st, cls, prefix_len, r_rev_bp, r_item_bp, window=0, stream=None):

@@ -240,6 +240,10 @@ struct rc_ctx {
   int32_t* sel_urow = nullptr;
   // tensor maps
   CUtensorMap mA_a{}, mA_o{}, mA_h{};
+  CUtensorMap mA_a64{}, mA_o64{}, mA_h64{};  // same operands, gemm_t_box_rows()-row boxes (transposed small-M GEMM)
+  // residual-GEMM workspace: partial tiles summed in K order (bitwise-reproducible residual stream)
+  float* gemm_ws = nullptr;
+  int* gemm_cnt = nullptr;
   CUtensorMap mC_x{}, mC_xs{};  // fp32 residual streams as TMA reduce-add targets
   std::vector<CUtensorMap> mB_qkv, mB_kv, mB_o, mB_gu, mB_d;
   CUtensorMap mB_lm{};
@@ -277,7 +281,7 @@ struct rc_ctx {
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
                     a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
-                    mass_lse, mass_a, attn_ctr};
+                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt};
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
@@ -309,6 +313,15 @@ cudaEvent_t next_ev(rc_ctx* c) {
       c->recs.push_back({kind, a_, b_, static_cast<double>(flops), static_cast<double>(bytes), pending}); \
     }                                                                                                   \
   } while (0)
+// every GEMM epilogue starts from the context's workspace (used by the residual epilogues)
+EpiArgs epi_base(const rc_ctx* c) {
+  EpiArgs e{};
+  e.ws = c->gemm_ws;
+  e.ws_cnt = c->gemm_cnt;
+  e.ws_slots = gemm_ws_slots();
+  e.head_dim = c->m.head_dim;
+  return e;
+}
 double gemm_flops(double M, double N, double K) { return 2.0 * M * N * K; }
 double gemm_bytes(double M, double N, double K, double out_b) { return (M * K + N * K) * 2.0 + M * N * out_b; }
 
@@ -445,23 +458,44 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
     c->ln2.push_back(static_cast<const uint16_t*>(w->ln2[l]));
     c->wo.push_back(static_cast<const uint16_t*>(w->wo[l]));
     c->wd.push_back(static_cast<const uint16_t*>(w->wd[l]));
+    // q | k | v heads; inside every head the rows in rotate-half pair order [0, dh/2, 1, dh/2+1, ...]
+    // (RoPE partners adjacent in every GEMM orientation, k_gemm.cu)
     uint16_t* dq = c->wqkv + static_cast<size_t>(l) * c->Nqkv * d;
-    RC_CUDA(cudaMemcpy(dq, w->wq[l], static_cast<size_t>(H) * dh * d * 2, cudaMemcpyDeviceToDevice));
-    RC_CUDA(cudaMemcpy(dq + static_cast<size_t>(H) * dh * d, w->wk[l], static_cast<size_t>(Hk) * dh * d * 2,
-                       cudaMemcpyDeviceToDevice));
-    RC_CUDA(cudaMemcpy(dq + static_cast<size_t>(H + Hk) * dh * d, w->wv[l], static_cast<size_t>(Hk) * dh * d * 2,
-                       cudaMemcpyDeviceToDevice));
+    const size_t row_b = static_cast<size_t>(d) * 2, half_b = static_cast<size_t>(dh / 2) * row_b;
+    auto pack_heads = [&](uint16_t* dst, const void* src, int nheads) -> cudaError_t {
+      for (int hh = 0; hh < nheads; ++hh) {
+        uint8_t* dh8 = reinterpret_cast<uint8_t*>(dst) + static_cast<size_t>(hh) * 2 * half_b;
+        const uint8_t* sh8 = static_cast<const uint8_t*>(src) + static_cast<size_t>(hh) * 2 * half_b;
+        cudaError_t e2 = cudaMemcpy2D(dh8, 2 * row_b, sh8, row_b, row_b, dh / 2, cudaMemcpyDeviceToDevice);
+        if (e2 == cudaSuccess) e2 = cudaMemcpy2D(dh8 + row_b, 2 * row_b, sh8 + half_b, row_b, row_b, dh / 2,
+                                                 cudaMemcpyDeviceToDevice);
+        if (e2 != cudaSuccess) return e2;
+      }
+      return cudaSuccess;
+    };
+    RC_CUDA(pack_heads(dq, w->wq[l], H));
+    RC_CUDA(pack_heads(dq + static_cast<size_t>(H) * dh * d, w->wk[l], Hk));
+    RC_CUDA(pack_heads(dq + static_cast<size_t>(H + Hk) * dh * d, w->wv[l], Hk));
     if (m.qkv_bias) {
       uint16_t* db = c->bqkv + static_cast<size_t>(l) * c->Nqkv;
-      RC_CUDA(cudaMemcpy(db, w->bq[l], static_cast<size_t>(H) * dh * 2, cudaMemcpyDeviceToDevice));
-      RC_CUDA(cudaMemcpy(db + H * dh, w->bk[l], static_cast<size_t>(Hk) * dh * 2, cudaMemcpyDeviceToDevice));
-      RC_CUDA(cudaMemcpy(db + (H + Hk) * dh, w->bv[l], static_cast<size_t>(Hk) * dh * 2, cudaMemcpyDeviceToDevice));
+      auto pack_bias = [&](uint16_t* dst, const void* src, int nheads) -> cudaError_t {
+        for (int hh = 0; hh < nheads; ++hh) {  // element pitch 2 bytes: even slots <- first half, odd <- second
+          uint16_t* dh16 = dst + static_cast<size_t>(hh) * dh;
+          const uint16_t* sh16 = static_cast<const uint16_t*>(src) + static_cast<size_t>(hh) * dh;
+          cudaError_t e2 = cudaMemcpy2D(dh16, 4, sh16, 2, 2, dh / 2, cudaMemcpyDeviceToDevice);
+          if (e2 == cudaSuccess) e2 = cudaMemcpy2D(dh16 + 1, 4, sh16 + dh / 2, 2, 2, dh / 2, cudaMemcpyDeviceToDevice);
+          if (e2 != cudaSuccess) return e2;
+        }
+        return cudaSuccess;
+      };
+      RC_CUDA(pack_bias(db, w->bq[l], H));
+      RC_CUDA(pack_bias(db + H * dh, w->bk[l], Hk));
+      RC_CUDA(pack_bias(db + (H + Hk) * dh, w->bv[l], Hk));
     }
-    // gate/up interleaved in 128-row chunks: [g 0..127 | u 0..127 | g 128..255 | u 128..255 | ...]
+    // gate/up interleaved by row: [g0, u0, g1, u1, ...]
     uint16_t* dg = c->wgu + static_cast<size_t>(l) * 2 * F * d;
-    const size_t chunk = static_cast<size_t>(128) * d * 2;
-    RC_CUDA(cudaMemcpy2D(dg, 2 * chunk, w->wg[l], chunk, chunk, F / 128, cudaMemcpyDeviceToDevice));
-    RC_CUDA(cudaMemcpy2D(reinterpret_cast<uint8_t*>(dg) + chunk, 2 * chunk, w->wu[l], chunk, chunk, F / 128,
+    RC_CUDA(cudaMemcpy2D(dg, 2 * row_b, w->wg[l], row_b, row_b, F, cudaMemcpyDeviceToDevice));
+    RC_CUDA(cudaMemcpy2D(reinterpret_cast<uint8_t*>(dg) + row_b, 2 * row_b, w->wu[l], row_b, row_b, F,
                          cudaMemcpyDeviceToDevice));
   }
   // pools + arena
@@ -522,10 +556,15 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   RC_CUDA(cudaMemset(c->o, 0, Mx * H * dh * 2));
   RC_CUDA(cudaMemset(c->h, 0, Mx * F * 2));
   // tensor maps: A operands (rows = Mx; tiles never read beyond the call's M-tile), B = weights
+  c->gemm_ws = dev_alloc<float>(gemm_ws_floats(), &e); if (e) return fail(RC_E_NOMEM, "gemm workspace");
+  c->gemm_cnt = dev_alloc<int>(2 * gemm_ws_slots(), &e); if (e) return fail(RC_E_NOMEM, "gemm workspace");
+  RC_CUDA(cudaMemset(c->gemm_cnt, 0, 2 * gemm_ws_slots() * sizeof(int)));
   bool ok = make_tmap_bf16_2d(&c->mA_a, c->a, Mx, d, d, 128) &&
             make_tmap_bf16_2d(&c->mA_o, c->o, Mx, H * dh, H * dh, 128) &&
             make_tmap_bf16_2d(&c->mA_h, c->h, Mx, F, F, 128) && make_tmap_f32_2d(&c->mC_x, c->x, Mx, d, d) &&
-            make_tmap_f32_2d(&c->mC_xs, c->xs, Mx, d, d);
+            make_tmap_f32_2d(&c->mC_xs, c->xs, Mx, d, d) && make_tmap_bf16_2d(&c->mA_a64, c->a, Mx, d, d, gemm_t_box_rows()) &&
+            make_tmap_bf16_2d(&c->mA_o64, c->o, Mx, H * dh, H * dh, gemm_t_box_rows()) &&
+            make_tmap_bf16_2d(&c->mA_h64, c->h, Mx, F, F, gemm_t_box_rows());
   c->bn_qkv = pick_bn(c->Nqkv);
   c->bn_kv = pick_bn(2 * Hk * dh);
   c->bn_o = pick_bn(d);
@@ -904,13 +943,12 @@ namespace {
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
 rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
                     const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min,
-                    bool paired,
-                    double attn_flops, int attn_pending, cudaStream_t s) {
+                    bool paired, double attn_flops, int attn_pending, int det, cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
   const double R = rows, norm_b = R * d * 6.0;
   RC_LAUNCH(RC_K_SMALL, 0, norm_b, -1, rmsnorm_launch(x, nullptr, rows, d, c->ln1[l], m.rms_eps, c->a, s));
-  EpiArgs ep{};
+  EpiArgs ep = epi_base(c);
   ep.bias = c->bqkv ? c->bqkv + static_cast<size_t>(l) * c->Nqkv : nullptr;
   ep.pos = d_pos; ep.dst_row = d_dst;
   ep.q_out = c->q; ep.q_ld = H * dh;
@@ -919,7 +957,8 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
   ep.rope_cos = c->rope_cos; ep.rope_sin = c->rope_sin; ep.rope_zero = c->rope_zero;
   ep.n_heads = H; ep.n_kv_heads = Hk; ep.head_dim = dh;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, c->Nqkv, d), gemm_bytes(R, c->Nqkv, d, 2), -1,
-            gemm_launch(&c->mA_a, &c->mB_qkv[l], nullptr, rows, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s));
+            gemm_launch(&c->mA_a, &c->mB_qkv[l], nullptr, rows, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s,
+                        &c->mA_a64));
   AttnArgs at{};
   at.q = c->q; at.o = c->o; at.qpos = d_pos; at.tiles = d_tiles; at.n_tiles = n_tiles;
   at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
@@ -962,19 +1001,22 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
               attn_tc_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
   else
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending, attn_launch(at, s));
-  EpiArgs eo{};
-  eo.out = x; eo.ldo = d;
+  EpiArgs eo = epi_base(c);
+  eo.out = x; eo.ldo = d; eo.det = det;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, H * dh), gemm_bytes(R, d, H * dh, 8), -1,
-            gemm_launch(&c->mA_o, &c->mB_o[l], mx, rows, d, H * dh, c->bn_o, EPI_ADD_F32, eo, c->num_sms, s));
+            gemm_launch(&c->mA_o, &c->mB_o[l], mx, rows, d, H * dh, c->bn_o, EPI_ADD_F32, eo, c->num_sms, s,
+                        &c->mA_o64));
   RC_LAUNCH(RC_K_SMALL, 0, norm_b, -1, rmsnorm_launch(x, nullptr, rows, d, c->ln2[l], m.rms_eps, c->a, s));
-  EpiArgs eg{};
+  EpiArgs eg = epi_base(c);
   eg.out = c->h; eg.ldo = F;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, 2.0 * F, d), gemm_bytes(R, 2.0 * F, d, 1), -1,
-            gemm_launch(&c->mA_a, &c->mB_gu[l], nullptr, rows, 2 * F, d, 256, EPI_SWIGLU, eg, c->num_sms, s));
-  EpiArgs ed{};
-  ed.out = x; ed.ldo = d;
+            gemm_launch(&c->mA_a, &c->mB_gu[l], nullptr, rows, 2 * F, d, 256, EPI_SWIGLU, eg, c->num_sms, s,
+                        &c->mA_a64));
+  EpiArgs ed = epi_base(c);
+  ed.out = x; ed.ldo = d; ed.det = det;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, F), gemm_bytes(R, d, F, 8), -1,
-            gemm_launch(&c->mA_h, &c->mB_d[l], mx, rows, d, F, c->bn_d, EPI_ADD_F32, ed, c->num_sms, s));
+            gemm_launch(&c->mA_h, &c->mB_d[l], mx, rows, d, F, c->bn_d, EPI_ADD_F32, ed, c->num_sms, s,
+                        &c->mA_h64));
   return RC_OK;
 }
 }  // namespace
@@ -1001,7 +1043,7 @@ rc_status mass_scores(rc_ctx* c, int cL, int32_t U, const int32_t* d_pos, const 
         !make_tmap_bf16_2d(&c->mV_mass, c->mass_v, static_cast<uint64_t>(Hk) * rows, dh, dh, 128))
       return fail(RC_E_CUDA, "attention-mass tensor maps");
   }
-  EpiArgs ep{};
+  EpiArgs ep = epi_base(c);
   ep.bias = c->bqkv ? c->bqkv + static_cast<size_t>(cL) * c->Nqkv : nullptr;
   ep.pos = d_pos; ep.dst_row = d_dst;
   ep.q_out = c->q; ep.q_ld = H * dh;
@@ -1010,7 +1052,8 @@ rc_status mass_scores(rc_ctx* c, int cL, int32_t U, const int32_t* d_pos, const 
   ep.rope_cos = c->rope_cos; ep.rope_sin = c->rope_sin; ep.rope_zero = c->rope_zero;
   ep.n_heads = H; ep.n_kv_heads = Hk; ep.head_dim = dh;
   RC_LAUNCH(RC_K_GEMM, gemm_flops(U, c->Nqkv, d), gemm_bytes(U, c->Nqkv, d, 2), -1,
-            gemm_launch(&c->mA_a, &c->mB_qkv[cL], nullptr, U, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s));
+            gemm_launch(&c->mA_a, &c->mB_qkv[cL], nullptr, U, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s,
+                        &c->mA_a64));
   for (auto& p : plan)  // the prefix keys are the exact cache: copy them next to the fresh U keys
     if (p.sq->P > 0)
       RC_LAUNCH(RC_K_SMALL, 0, 2.0 * p.sq->P * Hk * dh * 2, -1,
@@ -1181,7 +1224,9 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   attn_u *= 4.0 * m.n_heads * m.head_dim;
   const int pend_idx = c->prof ? static_cast<int>(c->pend.size()) : -1;
   for (int l = 0; l < cL; ++l) {
-    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, smin_u, pair_u, attn_u, -1, s);
+    // the layers < c decide Sel: their residual sums are always order-fixed (reproducible selection)
+    st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, smin_u, pair_u, attn_u, -1, 1,
+                   s);
     if (st != RC_OK) return st;
   }
   // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
@@ -1189,7 +1234,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     RC_CUDA(cudaMemsetAsync(c->dev, 0, static_cast<size_t>(U) * 8, s));
     RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(U) * d * 6.0, -1,
               rmsnorm_launch(c->x, nullptr, U, d, c->ln1[cL], m.rms_eps, c->a, s));
-    EpiArgs ev{};
+    EpiArgs ev = epi_base(c);
     ev.bias = c->bqkv ? c->bqkv + static_cast<size_t>(cL) * c->Nqkv + m.n_heads * m.head_dim : nullptr;
     ev.pos = D32(o_pos); ev.dst_row = D32(o_dst);
     ev.arena_k = arena_layer(c, cL, 0); ev.arena_v = arena_layer(c, cL, 1);
@@ -1224,7 +1269,8 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
             gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
   // ---- a5-a7: selective layers c..L-1 on Sel
   for (int l = cL; l < L; ++l) {
-    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, smin_s, pair_s, 0.0, pend_idx, s);
+    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, smin_s, pair_s, 0.0, pend_idx,
+                   prm->deterministic ? 1 : 0, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout
@@ -1240,7 +1286,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     }
     lg = c->logits;
   }
-  EpiArgs el{};
+  EpiArgs el = epi_base(c);
   el.out = lg; el.ldo = m.vocab;
   RC_LAUNCH(RC_K_LMHEAD, gemm_flops(n_req, m.vocab, d), gemm_bytes(n_req, m.vocab, d, 4), -1,
             gemm_launch(&c->mA_a, &c->mB_lm, nullptr, n_req, m.vocab, d, c->bn_lm, EPI_F32, el, c->num_sms, s));
@@ -1584,6 +1630,33 @@ rc_status rc_diag_gemm(int32_t M, int32_t N, int32_t K, const void* A, const voi
   EpiArgs ep{};
   ep.out = C; ep.ldo = N;
   RC_CUDA(gemm_launch(&ma, &mb, nullptr, M, N, K, bn, EPI_F32, ep, sms, static_cast<cudaStream_t>(stream)));
+  return RC_OK;
+}
+
+rc_status rc_diag_gemm_add(int32_t M, int32_t N, int32_t K, const void* A, const void* B, float* X, int32_t transposed,
+                           rc_stream stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !X || N % 32) return fail(RC_E_INVALID, "bad gemm args");
+  CUtensorMap ma, ma64, mb, mx;
+  if (!make_tmap_bf16_2d(&ma, A, M, K, K, 128) || !make_tmap_bf16_2d(&ma64, A, M, K, K, gemm_t_box_rows()) ||
+      !make_tmap_bf16_2d(&mb, B, N, K, K, gemm_box_rows_b(256)) || !make_tmap_f32_2d(&mx, X, M, N, N))
+    return fail(RC_E_CUDA, "tensor map encode failed");
+  int dev = 0, sms = 148;
+  RC_CUDA(cudaGetDevice(&dev));
+  RC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* ws = nullptr;
+  int* cnt = nullptr;
+  RC_CUDA(cudaMalloc(&ws, gemm_ws_floats() * sizeof(float)));
+  RC_CUDA(cudaMalloc(&cnt, 2 * gemm_ws_slots() * sizeof(int)));
+  RC_CUDA(cudaMemsetAsync(cnt, 0, 2 * gemm_ws_slots() * sizeof(int), s));
+  EpiArgs ep{};
+  ep.out = X; ep.ldo = N;
+  ep.ws = ws; ep.ws_cnt = cnt; ep.ws_slots = gemm_ws_slots();
+  cudaError_t e = gemm_launch(&ma, &mb, &mx, M, N, K, 256, EPI_ADD_F32, ep, sms, s, transposed ? &ma64 : nullptr);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(ws);
+  cudaFree(cnt);
+  if (e != cudaSuccess) return fail(RC_E_CUDA, std::string("diag gemm add: ") + cudaGetErrorString(e));
   return RC_OK;
 }
 

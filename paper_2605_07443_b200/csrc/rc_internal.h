@@ -40,8 +40,8 @@ enum EpiKind : int {
   EPI_BF16 = 0,     // out bf16 [M][ldo] (= acc + bias)
   EPI_F32 = 1,      // out f32  [M][ldo]
   EPI_ADD_F32 = 2,  // out f32  [M][ldo] += acc (residual stream)
-  EPI_SWIGLU = 3,   // N-tile = [128 gate | 128 up] -> out bf16 [M][ldo] = silu(g) * u
-  EPI_QKV = 4,      // packed [q | k | v] heads: RoPE at pos[row] on q,k; q -> q_out, k,v -> stitched arena
+  EPI_SWIGLU = 3,   // B rows [g0 u0 g1 u1 ...] -> out bf16 [M][ldo] = silu(g) * u
+  EPI_QKV = 4,      // packed [q | k | v] heads (dims [0, dh/2, 1, dh/2+1, ..]): RoPE at pos[row] on q,k; q -> q_out, k,v -> arena
   EPI_DEV = 5,      // packed [k | v] heads: RoPE on k, bf16 round, fixed-point |new - stitched| -> dev[row]
 };
 
@@ -62,13 +62,25 @@ struct EpiArgs {
   int32_t n_heads = 0, n_kv_heads = 0, head_dim = 0;
   unsigned long long* dev_out = nullptr;  // [M]
   const uint8_t* row_reuse = nullptr;     // [M]
+  // residual epilogues: workspace for partial tiles (split-K / stream-K) summed in K order by the
+  // last-arriving CTA of a tile (bitwise-reproducible x); counters zero between launches
+  float* ws = nullptr;      // gemm_ws_floats()
+  int* ws_cnt = nullptr;    // 2 * gemm_ws_slots()
+  int32_t ws_slots = 0;
+  int32_t det = 1;          // 0: partial tiles reduce-add straight into x in arrival order
 };
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
                        uint32_t box_rows);
 // c: output tensor map (fp32 [rows][cols], 32x32 SW128 boxes) for EPI_ADD_F32 (TMA reduce-add), else NULL
+// a64: optional map over the same A operand with gemm_t_box_rows()-row boxes; with it, small-M GEMMs
+// (QKV with head_dim 128, SwiGLU, residual; N % 256 == 0) run on the transposed CTA-pair kernel
 cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K, int bn,
-                        int epi, const EpiArgs& ep, int num_sms, cudaStream_t s);
+                        int epi, const EpiArgs& ep, int num_sms, cudaStream_t s, const CUtensorMap* a64 = nullptr);
+int gemm_t_box_rows();
+int gemm_ws_slots();
+size_t gemm_ws_floats();
+bool gemm_use_transposed(int M, int N, int epi, int head_dim, int num_sms);
 bool make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems);
 int gemm_box_rows_b(int bn);
 

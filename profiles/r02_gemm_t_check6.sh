@@ -1,0 +1,7 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "residual_gemm or gemm_matches or selective_prefill_parity or full_prefill or transposed" > gpurun_out/t_gemm.log 2>&1; echo gemm=$?
+tail -3 gpurun_out/t_gemm.log
+RC_GEMM_T=2 timeout 300 python bench.py --batch 1 --steps 30 --no-baselines --no-cpu-baseline > gpurun_out/b1_t2.log 2>&1; echo b1t2=$?
+timeout 300 python bench.py --batch 1 --steps 30 --no-baselines --no-cpu-baseline > gpurun_out/b1.log 2>&1; echo b1=$?
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active
+RC_GEMM_T=2 timeout 600 ncu --metrics $M --clock-control none -k "regex:^k_|k_gemm|k_attn" --csv --log-file gpurun_out/launches_b1_t2.csv python bench.py --profile-only --batch 1 --steps 1 --warmup 1 --no-baselines --no-cpu-baseline > /dev/null 2>&1; echo l1=$?

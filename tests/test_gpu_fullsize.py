@@ -73,12 +73,14 @@ def _setup(wl, batch, check_reqs):
                       for r in check_reqs}
     cand_off = np.concatenate([[0], np.cumsum([len(l["cand_idtok"]) for l in lays])])
     ctx.release(seqs)
-    # run-to-run determinism: the same batch assembled and prefilled again
-    seqs = ctx.assemble(lays, prefix_id=1, gather_from=C)
-    out2 = ctx.selective_prefill(seqs, R_BP, R_BP, check_layer=C, hidden=True, n_cand=n_cand)
-    torch.cuda.synchronize()
-    res["rerun"] = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out2.items()}
-    ctx.release(seqs)
+    # run-to-run determinism: the same batch assembled and prefilled again, in the default mode and
+    # twice with every residual sum order-fixed (deterministic=1)
+    for key, det in (("rerun", False), ("det1", True), ("det2", True)):
+        seqs = ctx.assemble(lays, prefix_id=1, gather_from=C)
+        out2 = ctx.selective_prefill(seqs, R_BP, R_BP, check_layer=C, hidden=True, n_cand=n_cand, deterministic=det)
+        torch.cuda.synchronize()
+        res[key] = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out2.items()}
+        ctx.release(seqs)
     ctx.close()
     Wh = {"embed": W["embed"].cpu(), "norm": W["norm"].cpu(), "lm_head": W["lm_head"].cpu(),
           "layers": [{k: v.cpu() for k, v in lw.items()} for lw in W["layers"]]}
@@ -147,14 +149,20 @@ def test_cfg3_batch32_request_matches_oracle(run, r):
 
 
 def test_cfg3_batch32_rerun_is_deterministic(run):
-    """The same batch twice (re-assembled): identical selection, logits and hidden states bit for bit."""
+    """The same batch again (re-assembled). Default mode: the layers < c, which decide Sel, sum their
+    partial tiles in K order, so the selection is identical; the later layers' split tiles meet in
+    arrival order, so logits may differ in the last bits (bounded here far below the parity tolerance).
+    deterministic=1: two runs are bitwise identical, and equal the default run's selection."""
     res, _ = run
-    rr = res["rerun"]
+    rr, d1, d2 = res["rerun"], res["det1"], res["det2"]
     assert np.array_equal(rr["sel_pos"], res["sel_pos"])
-    same = {k: bool(np.array_equal(rr[k], res[k])) for k in ("logits", "hidden", "cand_scores")}
-    diff = {k: float(np.max(np.abs(rr[k] - res[k]))) for k in ("logits", "hidden")}
-    print("rerun bitwise identical", json.dumps(same), "max |diff|", json.dumps(diff))
-    assert all(same.values()), (same, diff)
+    assert np.array_equal(d1["sel_pos"], res["sel_pos"]) and np.array_equal(d2["sel_pos"], res["sel_pos"])
+    drift = rel_l2(rr["logits"], res["logits"])
+    same = {k: bool(np.array_equal(d1[k], d2[k])) for k in ("logits", "hidden", "cand_scores")}
+    print("rerun: default-mode logits rel-L2 drift", drift, "deterministic bitwise", json.dumps(same))
+    assert drift < 1e-3
+    assert all(same.values()), same
+    assert rel_l2(d1["logits"], res["logits"]) < 1e-3
 
 
 def test_cfg3_batch32_logits_over_checked_set():

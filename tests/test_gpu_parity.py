@@ -51,6 +51,28 @@ def test_gemm_matches_exact_matmul(M, N, K, bn):
     assert np.max(np.abs(C - ref)) < 1e-3 * np.max(np.abs(ref)) + 1e-6
 
 
+@pytest.mark.parametrize("M,N,K,trans", [(625, 4096, 4096, True), (625, 4096, 14336, True), (113, 1024, 640, True),
+                                         (395, 512, 2048, True), (1000, 768, 4096, True), (3889, 4096, 4096, False),
+                                         (625, 4096, 14336, False), (200, 512, 4096, False), (4096, 1024, 1024, False)])
+def test_residual_gemm_exact_and_reproducible(M, N, K, trans):
+    """x += A B^T through every residual-GEMM schedule (transposed pair tiles with a ragged token tail,
+    split-K, the stream-K tail, whole tiles): equal to the exact product added to x, and bitwise the
+    same on a second run (partial tiles are summed in K order by the last-arriving CTA)."""
+    from paper_2605_07443_b200.api import diag_gemm_add
+    g = torch.Generator(device="cpu").manual_seed(M + 3 * N + K)
+    A = torch.randn((M, K), generator=g).to(torch.bfloat16)
+    B = (torch.randn((N, K), generator=g) / K ** 0.5).to(torch.bfloat16)
+    X0 = torch.randn((M, N), generator=g)
+    ref = X0.double().numpy() + A.double().numpy() @ B.double().numpy().T
+    outs = []
+    for _ in range(2):
+        X = X0.clone().cuda()
+        diag_gemm_add(A.cuda(), B.cuda(), X, transposed=trans)
+        outs.append(X.cpu().numpy())
+    assert rel_l2(outs[0], ref) < 3e-5 and np.max(np.abs(outs[0] - ref)) < 1e-3 * np.max(np.abs(ref))
+    assert np.array_equal(outs[0], outs[1])
+
+
 # ----------------------------------------------------------------------------- K2 gather
 @pytest.mark.parametrize("wl,gather_from", [(rcgen.CFG1, 1), (rcgen.CFG1_Q7, 1), (rcgen.CFG1, 0), (rcgen.MINI_L, 1),
                                              (rcgen.MINI_Q, 2)])
@@ -371,6 +393,37 @@ def test_attention_running_base_fallback(attn_kernel, tmp_path):
         e_spec = rel_l2(res["logits"][r], forced["logits"])
         e_ref = rel_l2(ref["logits"][r], forced["logits"])
         assert e_spec <= 1.1 * e_ref + 2e-3, (e_spec, e_ref)
+
+
+def _gemm_t_child(path):
+    wl = rcgen.MINI_L
+    case = make_case(wl, n_req=2)
+    pools = oracle_pools(case)
+    res, _ = _run_gpu(wl, case, pools, 1500)
+    np.savez(path, logits=res["logits"], hidden=res["hidden"], sel_pos=res["sel_pos"], sel_off=np.asarray(res["sel_off"]))
+
+
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_transposed_gemm_modes_match_oracle(mode, tmp_path):
+    """Every GEMM schedule choice end to end: RC_GEMM_T=1 puts the QKV (RoPE + K/V scatter), SwiGLU and
+    residual GEMMs of every layer on the transposed CTA-pair kernel, RC_GEMM_T=0 none of them (the knob
+    is read once per process: child process). Both must match O-SEL forced to their selection."""
+    import subprocess, sys, os
+    path = str(tmp_path / "gemm_t.npz")
+    code = ("import sys; sys.path.insert(0, %r); from tests.test_gpu_parity import _gemm_t_child; _gemm_t_child(%r)"
+            % (os.getcwd(), path))
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, RC_GEMM_T=mode), timeout=600)
+    z = np.load(path)
+    wl = rcgen.MINI_L
+    case = make_case(wl, n_req=2)
+    pools = oracle_pools(case)
+    off = z["sel_off"]
+    for r, lay in enumerate(layouts(case)):
+        sel = z["sel_pos"][off[r]:off[r + 1]]
+        forced, own = _oracle_forced(case, pools, lay, sel, 1500)
+        assert len(own["sel"]) == len(sel)
+        assert rel_l2(z["logits"][r], forced["logits"]) < TOL
+        assert rel_l2(z["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
 
 
 # ----------------------------------------------------------------------------- NEXT-1: attention mass
