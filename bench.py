@@ -47,6 +47,8 @@ def parse():
                     help="serving mode (SURVEY §8(d) config 4 on one GPU): open-loop Poisson arrivals at this rate, "
                          "dynamic batching up to --batch; reports TTFT p50/p99 (arrival -> logits on the device)")
     ap.add_argument("--requests", type=int, default=400, help="requests in the Poisson run")
+    ap.add_argument("--pools", default="materialized", choices=["materialized", "random"],
+                    help="pool contents: the model's own KV (R16/R17, default) or seeded random bytes")
     ap.add_argument("--host-frac", type=float, default=0.0,
                     help="NEXT-2: this fraction of the catalog lives only in the pinned host tier; each batch's "
                          "host-tier candidates are pulled by rc_fetch_host on a side stream during the previous batch")
@@ -122,7 +124,7 @@ def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
                 routed=[int((routes == p).sum()) for p in range(world)])
 
 
-def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_frac=0.0):
+def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_frac=0.0, pools="materialized"):
     import torch
     import rcgen
     from paper_2605_07443_b200.api import RcContext
@@ -156,27 +158,42 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_fr
                     prefix_rows=wl.prefix_len, arena_rows=batch * n, max_seq_len=n, max_batch_tokens=batch * n,
                     remote_rows=remote_rows, device=device.index or 0,
                     host_item_rows=len(host_items) * wl.item_len)
-    # item pool: this GPU's items (whole catalog at N=1), generated on the device in chunks and registered
-    chunk = 128
-    for i0 in range(0, len(items), chunk):
-        ids = items[i0:i0 + chunk]
-        kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
-        ctx.pool_register_blocks(R.RC_POOL_ITEM_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids),
-                                 kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
-        del kv
-    for i0 in range(0, len(host_items), chunk):  # NEXT-2 host tier (pinned DRAM, written over PCIe)
-        ids = host_items[i0:i0 + chunk]
-        kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
-        ctx.pool_register_blocks(R.RC_POOL_ITEM_HOST_BF16, ids, [wl.item_len] * len(ids),
-                                 [wl.prefix_len] * len(ids), kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
-        del kv
-    for i0 in range(0, len(used_protos), 4096):
-        ids = used_protos[i0:i0 + 4096]
-        q, s = rcgen.pools.hist_kv(shape, ids, device=device)
-        ctx.pool_register_blocks(R.RC_POOL_HIST_INT8, ids, [1] * len(ids), [int(protos.canon_pos[p]) for p in ids], q, s)
-        del q, s
-    ctx.pool_register_blocks(R.RC_POOL_PREFIX_BF16, [1], [wl.prefix_len], [0],
-                             rcgen.pools.prefix_kv(shape, wl.prefix_len, device=device))
+    if pools == "materialized":
+        # SURVEY §8(d) "Pool contents" (R16/R17): the pools hold the model's own KV -- the prefix by a full
+        # prefill of the system prompt, every item by a full prefill of [system prompt; item], every
+        # prototype at its canonical position in a review-corpus sequence, int8 (R15) -- so the Eq. 3
+        # deviations the selection ranks are real context drift (librc's dense path, materialize.py)
+        from paper_2605_07443_b200 import materialize as MZ
+        MZ.register_prefix(ctx, sys_tok, 1)
+        MZ.register_items(ctx, sys_tok, 1, items, [cat.tokens[i] for i in items])
+        if host_items:
+            MZ.register_items(ctx, sys_tok, 1, host_items, [cat.tokens[i] for i in host_items],
+                              kind=R.RC_POOL_ITEM_HOST_BF16)
+        corpus, seq_of, off_of = rcgen.proto_corpus(wl, protos, used_protos)
+        MZ.register_protos(ctx, sys_tok, 1, used_protos, [int(protos.canon_pos[p]) for p in used_protos], corpus,
+                           seq_of, off_of)
+    else:
+        # seeded random pool bytes (random-stand-in mode, --pools random)
+        chunk = 128
+        for i0 in range(0, len(items), chunk):
+            ids = items[i0:i0 + chunk]
+            kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
+            ctx.pool_register_blocks(R.RC_POOL_ITEM_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids),
+                                     kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
+            del kv
+        for i0 in range(0, len(host_items), chunk):  # NEXT-2 host tier (pinned DRAM, written over PCIe)
+            ids = host_items[i0:i0 + chunk]
+            kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=device)
+            ctx.pool_register_blocks(R.RC_POOL_ITEM_HOST_BF16, ids, [wl.item_len] * len(ids),
+                                     [wl.prefix_len] * len(ids), kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
+            del kv
+        for i0 in range(0, len(used_protos), 4096):
+            ids = used_protos[i0:i0 + 4096]
+            q, s = rcgen.pools.hist_kv(shape, ids, device=device)
+            ctx.pool_register_blocks(R.RC_POOL_HIST_INT8, ids, [1] * len(ids), [int(protos.canon_pos[p]) for p in ids], q, s)
+            del q, s
+        ctx.pool_register_blocks(R.RC_POOL_PREFIX_BF16, [1], [wl.prefix_len], [0],
+                                 rcgen.pools.prefix_kv(shape, wl.prefix_len, device=device))
     torch.cuda.synchronize(device)
     layouts = [ctx.decompose_prompt(sys_tok, r.hist_protos, r.hist_tokens, r.cand_items,
                                     [cat.tokens[int(i)] for i in r.cand_items], r.tail_tokens) for r in reqs]
@@ -381,7 +398,7 @@ def run_ours(args, wl):
         dist.all_gather_object(lst, obj)
         return lst
 
-    env = build_ours(wl, batch, args.distinct_batches, rank, device, world=world, gather=gather,
+    env = build_ours(wl, batch, args.distinct_batches, rank, device, world=world, gather=gather, pools=args.pools,
                      host_frac=args.host_frac)
     ctx, batches, fetch = env["ctx"], env["batches"], env["fetch"]
     n_cand = sum(len(l["cand_idtok"]) for l in batches[0])
@@ -532,7 +549,10 @@ def run_ours(args, wl):
            "config": {"workload": wl.name, "batch": batch, "seq_len": wl.n, "r": r_bp / 1e4, "check_layer": c,
                       "parallelism": (f"dp{world}: Alg. 1 sharded item pool, Eq. 2 routing, NVLink fetch"
                                       if world > 1 else "dp1"),
-                      "l2": "inputs larger than L2 (16 GB weights + item pool per GPU)"},
+                      "l2": "inputs larger than L2 (16 GB weights + item pool per GPU)",
+                      "pools": ("materialized by the model (R16/R17: item/prefix/prototype KV from librc full "
+                                "prefills, prototypes int8 per R15)" if args.pools == "materialized"
+                                else "seeded random pool bytes")},
            "ttft_ms": {"p50": float(np.percentile(step_ms, 50, method="inverted_cdf")),
                        "p99": float(np.percentile(step_ms, 99, method="inverted_cdf")),
                        "note": "batch mode: every request of a batch is submitted at the step start"},

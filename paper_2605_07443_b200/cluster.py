@@ -103,3 +103,26 @@ def plan_fetch(batch_candidates, resident_local, directory, rank):
             continue
         plan.append((it, owner, row))
     return plan
+
+
+def hit_accounting(requests, routes, resident, item_bytes):
+    """Per-request candidate classes under a placement: local (resident on the
+    routed GPU), peer (resident on another GPU: one NVLink pull), miss (resident nowhere: recomputed
+    as FORCED, or pulled from the host tier). Returns rates over all candidates, the fetch bytes per
+    request and the resident fraction of the catalog."""
+    k, n_items = resident.shape
+    anywhere = resident.any(axis=0)
+    loc = peer = miss = tot = 0
+    for items, g in zip(requests, routes):
+        items = np.asarray(items, np.int64)
+        l = resident[g][items].astype(bool)
+        a = anywhere[items]
+        loc += int(l.sum())
+        peer += int((a & ~l).sum())
+        miss += int((~a).sum())
+        tot += len(items)
+    per = [int((np.asarray(routes) == p).sum()) for p in range(k)]
+    return {"local_hit": loc / tot, "peer_hit": peer / tot, "miss": miss / tot,
+            "resident_frac": float(anywhere.mean()), "resident_per_gpu": [int(x) for x in resident.sum(axis=1)],
+            "fetch_mb_per_request": peer / len(requests) * item_bytes / 2 ** 20,
+            "routed": per, "route_imbalance": max(per) / max(1.0, np.mean(per))}

@@ -40,21 +40,26 @@ template <int V>
 __global__ void __launch_bounds__(256) k_rmsnorm(const float* __restrict__ x, const int32_t* __restrict__ row_idx,
                                                  int32_t d, const uint16_t* __restrict__ g, float eps,
                                                  uint16_t* __restrict__ out) {
-  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
-  griddep_launch();
   __shared__ float red[8];
   const int r = blockIdx.x;
-  const int64_t src = row_idx ? row_idx[r] : r;
-  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
   const uint2* grow = reinterpret_cast<const uint2*>(g);
   const int n4 = d / 4;
   float4 v[V];
   uint2 gg[V];
+  // the gains are weights (not produced by the previous kernel): fetched while it drains (PDL)
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    gg[k] = i < n4 ? __ldg(&grow[i]) : make_uint2(0u, 0u);
+  }
+  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
+  griddep_launch();
+  const int64_t src = row_idx ? row_idx[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
 #pragma unroll
   for (int k = 0; k < V; ++k) {
     const int i = threadIdx.x + k * blockDim.x;
     v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    gg[k] = i < n4 ? __ldg(&grow[i]) : make_uint2(0u, 0u);
   }
   float ss = 0.f;
 #pragma unroll

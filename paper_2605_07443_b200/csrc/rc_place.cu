@@ -198,8 +198,10 @@ rc_status rc_place_items(int32_t n_items, const int32_t* item_tokens, int32_t n_
   for (int j = 0; j < n_hot; ++j) hot[order[j]] = 1;
   for (int i = 0; i < n_items; ++i)
     if (!hot[i]) { cold_id[i] = static_cast<int>(cold.size()); cold.push_back(i); }
-  // Phase 3-4: co-occurrence graph over cold items (same historical request)
-  std::vector<std::tuple<int, int, int64_t>> edges;
+  // Phase 3-4: co-occurrence graph over cold items (same historical request): every co-occurring
+  // pair as one 64-bit key (u << 32 | v, u < v), sorted, runs counted = edge weights (8 bytes per
+  // pair occurrence: a 1M-item catalog with a 50K-request trace is ~60M pairs)
+  std::vector<uint64_t> keys;
   std::vector<int> tmp;
   for (int r = 0; r < n_hist; ++r) {
     tmp.clear();
@@ -208,16 +210,19 @@ rc_status rc_place_items(int32_t n_items, const int32_t* item_tokens, int32_t n_
     std::sort(tmp.begin(), tmp.end());
     tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
     for (size_t a = 0; a < tmp.size(); ++a)
-      for (size_t b = a + 1; b < tmp.size(); ++b) edges.emplace_back(tmp[a], tmp[b], 1);
+      for (size_t b = a + 1; b < tmp.size(); ++b)
+        keys.push_back(static_cast<uint64_t>(tmp[a]) << 32 | static_cast<uint32_t>(tmp[b]));
   }
-  std::sort(edges.begin(), edges.end());
+  std::sort(keys.begin(), keys.end());
   std::vector<std::tuple<int, int, int64_t>> merged;
-  for (auto& e : edges) {
-    if (!merged.empty() && std::get<0>(merged.back()) == std::get<0>(e) && std::get<1>(merged.back()) == std::get<1>(e))
-      std::get<2>(merged.back()) += 1;
-    else
-      merged.push_back(e);
+  for (size_t i = 0; i < keys.size();) {
+    size_t j = i;
+    while (j < keys.size() && keys[j] == keys[i]) ++j;
+    merged.emplace_back(static_cast<int>(keys[i] >> 32), static_cast<int>(keys[i] & 0xffffffffu),
+                        static_cast<int64_t>(j - i));
+    i = j;
   }
+  std::vector<uint64_t>().swap(keys);
   std::vector<int64_t> w(cold.size());
   for (size_t c = 0; c < cold.size(); ++c) w[c] = item_tokens[cold[c]];
   Graph g = build_csr(static_cast<int>(cold.size()), w, merged);

@@ -36,7 +36,7 @@ _LOGITS = {}
 CHECK_REQS = tuple(int(x) for x in os.environ.get("RC_FULLSIZE_REQS", "0,31").split(","))
 
 
-def _setup(wl, batch, check_reqs):
+def _setup(wl, batch, check_reqs, materialize=False):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2605_07443_b200.build import build
@@ -53,15 +53,26 @@ def _setup(wl, batch, check_reqs):
     n = wl.n
     ctx = RcContext(shape, W, item_rows=len(items) * wl.item_len, hist_rows=len(pids), prefix_rows=wl.prefix_len,
                     arena_rows=batch * n, max_seq_len=n, max_batch_tokens=batch * n)
-    for i0 in range(0, len(items), 128):
-        ids = items[i0:i0 + 128]
-        kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=dev)
-        ctx.pool_register_blocks(R.RC_POOL_ITEM_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids),
-                                 kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
-    hq, hs = rcgen.pools.hist_kv(shape, pids, device=dev)
-    ctx.pool_register_blocks(R.RC_POOL_HIST_INT8, pids, [1] * len(pids), [int(protos.canon_pos[p]) for p in pids], hq, hs)
-    pkv = rcgen.pools.prefix_kv(shape, wl.prefix_len, device=dev)
-    ctx.pool_register_blocks(R.RC_POOL_PREFIX_BF16, [1], [wl.prefix_len], [0], pkv)
+    item_kv = None
+    if materialize:  # SURVEY §8(d) "Pool contents": the model's own KV (R16/R17, int8 prototypes per R15)
+        from paper_2605_07443_b200 import materialize as MZ
+        pkv = MZ.register_prefix(ctx, sys_tok, 1)
+        item_kv = {i: v.cpu() for i, v in MZ.register_items(ctx, sys_tok, 1, items, [cat.tokens[i] for i in items],
+                                                            keep=True).items()}
+        corpus, seq_of, off_of = rcgen.proto_corpus(wl, protos, pids)
+        hq, hs = MZ.register_protos(ctx, sys_tok, 1, pids, [int(protos.canon_pos[p]) for p in pids], corpus, seq_of,
+                                    off_of)
+    else:
+        for i0 in range(0, len(items), 128):
+            ids = items[i0:i0 + 128]
+            kv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=dev)
+            ctx.pool_register_blocks(R.RC_POOL_ITEM_BF16, ids, [wl.item_len] * len(ids), [wl.prefix_len] * len(ids),
+                                     kv.reshape(len(ids) * wl.item_len, *kv.shape[2:]))
+        hq, hs = rcgen.pools.hist_kv(shape, pids, device=dev)
+        ctx.pool_register_blocks(R.RC_POOL_HIST_INT8, pids, [1] * len(pids), [int(protos.canon_pos[p]) for p in pids],
+                                 hq, hs)
+        pkv = rcgen.pools.prefix_kv(shape, wl.prefix_len, device=dev)
+        ctx.pool_register_blocks(R.RC_POOL_PREFIX_BF16, [1], [wl.prefix_len], [0], pkv)
     lays = [ctx.decompose_prompt(sys_tok, r.hist_protos, r.hist_tokens, r.cand_items,
                                  [cat.tokens[int(i)] for i in r.cand_items], r.tail_tokens) for r in reqs]
     seqs = ctx.assemble(lays, prefix_id=1, gather_from=C)
@@ -86,7 +97,7 @@ def _setup(wl, batch, check_reqs):
           "layers": [{k: v.cpu() for k, v in lw.items()} for lw in W["layers"]]}
     hist = {p: (hq[j].cpu().numpy(), hs[j].cpu().numpy(), int(protos.canon_pos[p])) for j, p in enumerate(pids)}
     ctxd = dict(wl=wl, shape=shape, W=Wh, cat=cat, sys=sys_tok, reqs=reqs, items=items, hist=hist,
-                pkv=pkv.cpu(), cand_off=cand_off)
+                pkv=pkv.cpu(), cand_off=cand_off, item_kv=item_kv)
     del W
     torch.cuda.empty_cache()
     return res, ctxd
@@ -102,8 +113,11 @@ def _oracle(d, r, sel):
     req = d["reqs"][r]
     lay = layout_from_request(req, d["cat"], d["sys"])
     ids = [int(i) for i in req.cand_items]
-    ikv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=torch.device("cuda", 0)).cpu()
-    item_d = {it: (ikv[j], wl.prefix_len) for j, it in enumerate(ids)}
+    if d.get("item_kv") is not None:   # materialised pools: the registered bytes
+        item_d = {it: (d["item_kv"][it], wl.prefix_len) for it in ids}
+    else:
+        ikv = rcgen.pools.item_kv(shape, wl.item_len, ids, device=torch.device("cuda", 0)).cpu()
+        item_d = {it: (ikv[j], wl.prefix_len) for j, it in enumerate(ids)}
     K, V, dfn = assemble(shape, lay, item_d, d["hist"], d["pkv"], gather_from=C)
     forced = selective_prefill(OracleModel(shape, d["W"]), lay, K, V, R_BP, R_BP, check_layer=C, forced_sel=sel)
     # own selection from the 2-layer truncation (Sel is decided at the check layer c = 1)
@@ -214,5 +228,24 @@ def test_batch1_request_matches_oracle(wl):
            "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
            "K_last": rel_l2(Kg, forced["K"][L - 1][sel])}
     print(f"fullsize {wl.name} batch-1 parity", json.dumps(err))
+    assert jac >= 0.95, err
+    assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
+
+
+def test_cfg3_batch1_materialized_pools_matches_oracle():
+    """BASELINE configs[2] prompt at batch 1 on pools the model materialised itself (R16/R17; item and
+    prefix KV from full prefills, prototypes int8 at their canonical positions): the deviation scores
+    now measure real context drift. Same bounds as on the seeded pools; the Jaccard is reported."""
+    res, d = _setup(rcgen.CFG3, 1, (0,), materialize=True)
+    r = 0
+    off = res["sel_off"]
+    sel = res["sel_pos"][off[r]:off[r + 1]]
+    lay, K_asm, dfn, forced, own = _oracle(d, r, sel)
+    jac = len(set(own["sel"].tolist()) & set(sel.tolist())) / len(set(own["sel"].tolist()) | set(sel.tolist()))
+    Kg = bf16_to_f32(res["kv_last"][r][0])[sel].astype(np.float64)
+    err = {"jaccard": jac, "logits": rel_l2(res["logits"][r], forced["logits"]),
+           "hidden": rel_l2(res["hidden"][off[r]:off[r + 1]], forced["x_sel"]),
+           "K_last": rel_l2(Kg, forced["K"][d["shape"].n_layers - 1][sel])}
+    print("fullsize cfg3 batch-1 materialised-pool parity", json.dumps(err))
     assert jac >= 0.95, err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err

@@ -129,3 +129,36 @@ def test_percentile_and_capacity_goldens(golden):
     assert [O.percentile_nearest_rank(v, q) for q in (50, 90, 99)] == [g["p50"], g["p90"], g["p99"]]
     c = golden("capacity_spec173.json")
     assert c["items"] * c["tokens_per_item"] * c["bytes_per_token"] / 1e9 == c["expected_gb"]
+
+
+def test_config4_logical_scale_accounting_invariants():
+    """SURVEY §8(e) / R27 accounting (profiles/config4_scale.py) on a reduced catalog: capacity-bounded
+    resident sets (hot replicas first), Eq. 2 routing, local / peer / miss rates. The classes partition
+    the candidates, no GPU holds more than its capacity, the hot replicas are resident everywhere, the
+    resident fraction grows with k, and a catalog that fits entirely leaves no misses."""
+    from paper_2605_07443_b200 import cluster
+    from rcgen.catalog_scale import gen_catalog_struct, gen_candidate_lists
+    cs = gen_catalog_struct(20_000, 200)
+    hist = gen_candidate_lists(cs, 1500, 50, start=5_000_000)
+    reqs = gen_candidate_lists(cs, 400, 50)
+    tok = np.full(cs.n_items, 64, np.int32)
+    prev = 0.0
+    for k in (1, 2, 4):
+        part, cut, heat = cluster.place_items(tok, [h.tolist() for h in hist], k, hot_bp=10)
+        res = cluster.resident_matrix(part, k, heat, tok, capacity_tokens=3000 * 64)
+        routes, _ = cluster.route([r.tolist() for r in reqs], [4096] * len(reqs), res)
+        acc = cluster.hit_accounting(reqs, routes, res, 8 << 20)
+        assert abs(acc["local_hit"] + acc["peer_hit"] + acc["miss"] - 1.0) < 1e-12
+        assert max(acc["resident_per_gpu"]) <= 3000
+        hot = np.nonzero(part == -1)[0]
+        assert len(hot) == 20 and res[:, hot].all()             # top 0.1 % replicated on every GPU
+        assert acc["resident_frac"] >= prev
+        prev = acc["resident_frac"]
+        if k == 1:
+            assert acc["peer_hit"] == 0.0                         # no peer with one GPU
+    # everything fits: no misses, and every candidate is local or one NVLink pull away
+    part, cut, heat = cluster.place_items(tok, [h.tolist() for h in hist], 2, hot_bp=10)
+    res = cluster.resident_matrix(part, 2, heat, tok)
+    routes, _ = cluster.route([r.tolist() for r in reqs], [4096] * len(reqs), res)
+    acc = cluster.hit_accounting(reqs, routes, res, 8 << 20)
+    assert acc["miss"] == 0.0 and acc["resident_frac"] == 1.0
