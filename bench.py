@@ -39,8 +39,12 @@ def parse():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--r-bp", type=int, default=0)
     ap.add_argument("--check-layer", type=int, default=1)
+    ap.add_argument("--lam", type=float, default=1.0,
+                    help="Eq. 3 lambda: 1 = deviation only (default, R3); < 1 adds the attention-mass term (NEXT-1)")
     ap.add_argument("--distinct-batches", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--flashinfer", action="store_true",
+                    help="also time the full prefill with flashinfer's prefill attention (JIT-compiles on first use)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no baselines, no oracle)")
     ap.add_argument("--poisson-qps", type=float, default=0.0,
@@ -124,7 +128,8 @@ def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
                 routed=[int((routes == p).sum()) for p in range(world)])
 
 
-def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_frac=0.0, pools="materialized"):
+def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_frac=0.0, pools="materialized",
+               mix=None):
     import torch
     import rcgen
     from paper_2605_07443_b200.api import RcContext
@@ -140,7 +145,10 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_fr
         items = np.nonzero(shard["res"][rank])[0].tolist()
         remote_rows = batch * wl.n_cand * wl.item_len
     else:
-        reqs = rcgen.gen_requests(wl, cat, protos, batch * n_batches, start=rank * 1_000_000)
+        if mix is not None:  # mixed prompt lengths over one catalog
+            _, reqs = rcgen.gen_mixed_requests(mix, cat, protos, batch * n_batches, start=rank * 1_000_000)
+        else:
+            reqs = rcgen.gen_requests(wl, cat, protos, batch * n_batches, start=rank * 1_000_000)
         items = list(range(wl.n_items))
         remote_rows = 0
     host_items = []
@@ -224,8 +232,10 @@ def host_bytes(batch_layouts):
 
 
 # --------------------------------------------------------------------------- torch full-prefill baseline
-def torch_full_prefill_ms(W, shape, tokens, reps=2):
-    """Full bf16 prefill in plain torch (cuBLAS GEMMs + SDPA flash attention) of [B][n] tokens."""
+def torch_full_prefill_ms(W, shape, tokens, reps=2, attn="sdpa"):
+    """Full bf16 prefill in plain torch (cuBLAS GEMMs + SDPA flash attention) of [B][n] tokens;
+    attn="flashinfer": the attention by flashinfer's prefill kernel (single_prefill_with_kv_cache,
+    causal, GQA) -- the library prefill baseline of SURVEY §8(d)."""
     import torch
     import torch.nn.functional as F
     dev = W["embed"].device
@@ -253,7 +263,13 @@ def torch_full_prefill_ms(W, shape, tokens, reps=2):
             q = rope(q.view(B, n, H, dh).transpose(1, 2))
             k = rope(k.view(B, n, Hk, dh).transpose(1, 2))
             v = v.view(B, n, Hk, dh).transpose(1, 2)
-            o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+            if attn == "flashinfer":
+                import flashinfer
+                o = torch.stack([flashinfer.single_prefill_with_kv_cache(
+                    q[b].transpose(0, 1).contiguous(), k[b].transpose(0, 1).contiguous(),
+                    v[b].transpose(0, 1).contiguous(), causal=True) for b in range(B)]).transpose(1, 2)
+            else:
+                o = F.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
             x = x + o.transpose(1, 2).reshape(B, n, H * dh) @ lw["wo"].T
             m = rms(x, lw["ln2"])
             g, u = (m @ wgu[l].T).split([shape.d_ff, shape.d_ff], -1)
@@ -364,7 +380,7 @@ def run_reference(args, wl):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators)",
            "config": {"workload": wl.name, "batch": args.batch or wl.batch, "seq_len": wl.n, "r": r_bp / 1e4,
-                      "check_layer": args.check_layer, "parallelism": "dp1",
+                      "check_layer": args.check_layer, "lambda": args.lam, "parallelism": "dp1",
                       "sample": "each step = one request of the batch (the oracle serves requests one at a time; "
                                 "tok/s is independent of the batch size)"},
            "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -399,7 +415,7 @@ def run_ours(args, wl):
         return lst
 
     env = build_ours(wl, batch, args.distinct_batches, rank, device, world=world, gather=gather, pools=args.pools,
-                     host_frac=args.host_frac)
+                     host_frac=args.host_frac, mix=args.mix)
     ctx, batches, fetch = env["ctx"], env["batches"], env["fetch"]
     n_cand = sum(len(l["cand_idtok"]) for l in batches[0])
     out_bufs = {"logits": torch.empty((batch, wl.shape.vocab), dtype=torch.float32, device=device),
@@ -442,7 +458,7 @@ def run_ours(args, wl):
             side.wait_stream(stream)
             fetch_host(i + 1)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
-                              out=out, stream=stream)
+                              out=out, stream=stream, lam=args.lam)
         ctx.release(seqs)
 
     for i in range(args.warmup):
@@ -497,7 +513,9 @@ def run_ours(args, wl):
         step(args.warmup + i)
     torch.cuda.synchronize(device)
     prof = ctx.profile_end()
-    tokens_all = batch * wl.n * args.steps * world
+    # prompt tokens per step: every request's n (mixed-length batches cycle through their batches)
+    tok_per_step = [sum(len(l["tokens"]) for l in batches[(args.warmup + i) % len(batches)]) for i in range(args.steps)]
+    tokens_all = sum(tok_per_step) * world
     value = tokens_all / (max_ms / 1e3)
 
     # ---- e2e through the public API: host request arrays in, logits + candidate scores to pinned host
@@ -546,7 +564,10 @@ def run_ours(args, wl):
     res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded generators, random-init weights)",
-           "config": {"workload": wl.name, "batch": batch, "seq_len": wl.n, "r": r_bp / 1e4, "check_layer": c,
+           "config": {"workload": args.config if args.mix else wl.name, "batch": batch,
+                      "seq_len": ("mixed " + "/".join(f"{w.n}:{f:.0%}" for w, f in args.mix)) if args.mix else wl.n,
+                      "r": r_bp / 1e4, "check_layer": c,
+                      "lambda": args.lam,
                       "parallelism": (f"dp{world}: Alg. 1 sharded item pool, Eq. 2 routing, NVLink fetch"
                                       if world > 1 else "dp1"),
                       "l2": "inputs larger than L2 (16 GB weights + item pool per GPU)",
@@ -620,15 +641,20 @@ def baselines(args, wl, env, r_bp, c, step_ms):
             lays = [dict(l, cls=np.full_like(l["cls"], 1)) for l in lays]  # every token FORCED, no prefix reuse
         seqs = ctx.assemble(lays, prefix_id=1, gather_from=c)
         n_cand = sum(len(l["cand_idtok"]) for l in lays)
-        ctx.selective_prefill(seqs, rbp, rbp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand)
+        ctx.selective_prefill(seqs, rbp, rbp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
+                              lam=args.lam if rbp < 10000 else 1.0)
         ctx.release(seqs)
 
     B = len(batches[0])
     full_ours = timed(lambda: run(batches[0], 10000, full=True), 2)
     out["full_prefill_ours_ms"] = float(np.median(full_ours))
-    tok = torch.tensor(np.stack([l["tokens"] for l in batches[0]]), device=W["embed"].device, dtype=torch.long)
+    toks = [torch.tensor(l["tokens"], device=W["embed"].device, dtype=torch.long)[None] for l in batches[0]]
+    tok = torch.cat(toks) if len({t.shape[1] for t in toks}) == 1 else None
     try:
-        out["full_prefill_torch_ms"] = torch_full_prefill_ms(W, wl.shape, tok, reps=2)
+        if tok is not None:
+            out["full_prefill_torch_ms"] = torch_full_prefill_ms(W, wl.shape, tok, reps=2)
+        else:  # mixed lengths: one dense prefill per request, back to back
+            out["full_prefill_torch_ms"] = float(sum(torch_full_prefill_ms(W, wl.shape, t, reps=1) for t in toks))
     except Exception as ex:
         out["full_prefill_torch_error"] = repr(ex)
     sel_ms = float(np.median(step_ms))
@@ -641,7 +667,13 @@ def baselines(args, wl, env, r_bp, c, step_ms):
     # the paper's own baseline: Prefix-Cache = the exact 207-token system prefix
     # reused, every other token recomputed (our path at r = 100%: Sel = U)
     pc1 = timed(lambda: run(one, 10000), 5)
-    t1 = torch_full_prefill_ms(W, wl.shape, tok[:1], reps=5)
+    t1 = torch_full_prefill_ms(W, wl.shape, toks[0], reps=5)
+    if args.flashinfer:
+        try:
+            out["full_flashinfer_b1_ms"] = torch_full_prefill_ms(W, wl.shape, toks[0], reps=5, attn="flashinfer")
+            t1 = min(t1, out["full_flashinfer_b1_ms"])
+        except Exception as ex:  # reported, never silently dropped
+            out["full_flashinfer_error"] = repr(ex)[:300]
     out["ttft_b1_ms"] = {"selective_p50": float(np.percentile(s1, 50, method="inverted_cdf")),
                          "selective_p99": float(np.percentile(s1, 99, method="inverted_cdf")),
                          "full_ours_p50": float(np.median(f1)), "full_torch_p50": t1,
@@ -779,7 +811,14 @@ def main():
         import faulthandler
         faulthandler.dump_traceback_later(int(os.environ["RC_WATCHDOG"]), exit=True)
     import rcgen
-    wl = rcgen.WORKLOADS[args.config]
+    if args.config in rcgen.MIXED:  # mixed-length batch: the longest class sizes the context
+        args.mix = rcgen.MIXED[args.config]
+        wl = max((w for w, _ in args.mix), key=lambda w: w.n)
+        args.batch = args.batch or 20
+        args.no_cpu_baseline = True
+    else:
+        args.mix = None
+        wl = rcgen.WORKLOADS[args.config]
     if args.impl == "reference":
         run_reference(args, wl)
     elif args.poisson_qps > 0:

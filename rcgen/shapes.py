@@ -81,9 +81,14 @@ CFG2 = Workload("cfg2-llama-1k", LLAMA3_8B, 207, 1024, 20, 64, 49, 4096, 256, 10
 CFG3 = Workload("cfg3-llama-4k", LLAMA3_8B, 207, 640, 50, 64, 49, 4096, 256, 100_000, 32)
 CFG5 = Workload("cfg5-qwen-8k", QWEN2_7B, 207, 1536, 100, 64, 49, 8192, 256, 100_000, 1)
 
+# config 5 mixed batch: 55 % 2560, 35 % 4096, 10 % 8192 tokens on the Qwen2 shape, one catalog
+CFG5_2560 = Workload("cfg5-qwen-2560", QWEN2_7B, 207, 1024, 20, 64, 49, 8192, 256, 100_000, 1)
+CFG5_4096 = Workload("cfg5-qwen-4096", QWEN2_7B, 207, 640, 50, 64, 49, 8192, 256, 100_000, 1)
 MINI_L = Workload("mini-llama", MINI_LLAMA, 64, 160, 8, 32, 16, 256, 16, 2048, 2)
 MINI_Q = Workload("mini-qwen", MINI_QWEN, 64, 160, 8, 32, 16, 256, 16, 2048, 2)
 
-WORKLOADS = {w.name: w for w in (CFG1, CFG1_Q7, CFG2, CFG3, CFG5, MINI_L, MINI_Q)}
+WORKLOADS = {w.name: w for w in (CFG1, CFG1_Q7, CFG2, CFG3, CFG5, CFG5_2560, CFG5_4096, MINI_L, MINI_Q)}
+MIXED = {"cfg5-mixed": ((CFG5_2560, 0.55), (CFG5_4096, 0.35), (CFG5, 0.10))}
 
 assert CFG1.n == 144 and CFG2.n == 2560 and CFG3.n == 4096 and CFG5.n == 8192
+assert CFG5_2560.n == 2560 and CFG5_4096.n == 4096

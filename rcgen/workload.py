@@ -169,3 +169,18 @@ def proto_corpus(wl: Workload, protos: Protos, proto_ids, seed: int = 4):
     toks = rng.integers(0, _free_vocab(wl), size=(S, H)).astype(np.int32)
     toks[seq, off] = protos.token[ids]
     return toks, seq, off.astype(np.int32)
+
+
+def gen_mixed_requests(mix, cat: Catalog, protos: Protos, n: int, start: int = 0):
+    """A mixed-length batch: n requests whose length classes follow the mix
+    fractions (largest remainder, classes interleaved in a seeded order); request i is generated by its
+    class's workload with seed 1000 + start + i over one shared catalog and prototype library.
+    Returns (workload per request, requests)."""
+    counts = [int(f * n) for _, f in mix]
+    rem = sorted(range(len(mix)), key=lambda j: -(mix[j][1] * n - counts[j]))
+    for j in rem[:n - sum(counts)]:
+        counts[j] += 1
+    cls = np.concatenate([np.full(c, j) for j, c in enumerate(counts)])
+    cls = cls[np.random.Generator(np.random.PCG64(5)).permutation(n)]
+    wls = [mix[int(j)][0] for j in cls]
+    return wls, [gen_request(w, cat, protos, start + i) for i, w in enumerate(wls)]
