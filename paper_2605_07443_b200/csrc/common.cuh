@@ -1,6 +1,7 @@
 // Device-side helpers for librc (sm_100a only): bf16 conversion, mbarrier, TMA and tcgen05
 // PTX wrappers. Kernel files include this; nothing here is shared with oracle/.
 #pragma once
+#define RC_COMMON_CUH 1
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -292,6 +293,11 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// arrive on an mbarrier once every cp.async this thread issued so far has completed (counts toward the
+// barrier's expected arrivals; the thread does not wait)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");

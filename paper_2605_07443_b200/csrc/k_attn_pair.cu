@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < KST; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
-    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < VST; ++i) { mbar_init(&v_full[i], a.vsrc.vmap ? 32 : 1); mbar_init(&v_empty[i], 1); }
     // p_full / o_free: one arrival per softmax warp of the tile (lane 0 after __syncwarp)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1); mbar_init(&p_full[t], 4); mbar_init(&o_done[t], 1); mbar_init(&o_free[t], 4);
@@ -162,7 +162,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {  // ---- V producer
+    if (a.vsrc.vmap != nullptr) {  // ---- V producer, zero-copy (NEXT-4): rows through vmap, 4 per lane
+      int vc = 0;
+      for (int i = 0;; ++i) {
+        const int w = next_item(i, true);
+        if (w < 0) break;
+        const Item it = decode(w);
+        for (int j = 0; j < it.nkv; ++j, ++vc) {
+          const int s = vc % VST;
+          mbar_wait(&v_empty[s], ((vc / VST) & 1) ^ 1);
+          v_rows_cp_async(sV + s * TILE, a.vsrc, a.v, a.head_stride,
+                          static_cast<int64_t>(it.kv_base) + static_cast<int64_t>(j) * BKV, it.kvh, t_cap);
+          cp_async_mbar_arrive(&v_full[s]);  // arrives when this lane's copies land (no wait here)
+        }
+      }
+    } else if (lane == 0) {  // ---- V producer
       tma_prefetch_desc(&tmV);
       int vc = 0;
       for (int i = 0;; ++i) {
@@ -213,6 +227,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int j = 0; j < it.nkv; ++j) {
           const int v = (vc + j) % VST;
           mbar_wait(&v_full[v], ((vc + j) / VST) & 1);
+          if (a.vsrc.vmap) fence_proxy_async();  // zero-copy V: cp.async (generic proxy) writes -> MMA reads
           tc_fence_after();
           bool k_ready = false;
 #pragma unroll

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < KST; ++i) mbar_init(&k_full[i], 1);
-    for (int i = 0; i < VST; ++i) mbar_init(&v_full[i], 1);
+    for (int i = 0; i < VST; ++i) mbar_init(&v_full[i], a.vsrc.vmap ? 32 : 1);  // zero-copy V: one per lane
     for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&pv_done[i], 1); }
     for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 4);  // p_full: 1 per warp
     fence_barrier_init();
@@ -114,7 +114,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 3) {
-    if (lane == 0) {  // ---- V producer
+    if (a.vsrc.vmap != nullptr) {  // ---- V producer, zero-copy (NEXT-4): rows through vmap, 4 per lane
+      const int64_t row0 = static_cast<int64_t>(kv_base) + static_cast<int64_t>(j0) * BKV;
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % VST;
+        mbar_wait(&pv_done[s], ((j / VST) & 1) ^ 1);  // PV_{j-2} complete: slot s is free
+        v_rows_cp_async(sV + s * TILE, a.vsrc, a.v, a.head_stride, row0 + static_cast<int64_t>(j) * BKV, kvh, t_cap);
+        cp_async_mbar_arrive(&v_full[s]);  // arrives when this lane's copies land (no wait here)
+      }
+    } else if (lane == 0) {  // ---- V producer
       tma_prefetch_desc(&tmV);
       const int vrow0 = static_cast<int>(kvh * t_cap + kv_base) + j0 * BKV;
       for (int j = 0; j < nkv; ++j) {
@@ -149,6 +157,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int j = 0; j < nkv; ++j) {
         const int b = j & 1, v = j % VST;
         mbar_wait(&v_full[v], (j / VST) & 1);
+        if (a.vsrc.vmap) fence_proxy_async();  // zero-copy V: cp.async (generic proxy) writes -> MMA reads
         for (int h = 0; h < 2; ++h) {
           mbar_wait(&p_full[b * 2 + h], (j >> 1) & 1);
           tc_fence_after();

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) k_gather(const GatherArgs g) {
     const int j = (u % CPR) * 8;
     const int4 m = __ldg(&g.meta[t]);
     if (m.w == KIND_FORCED) continue;  // recomputed later
+    if (g.skip_pool_v && kv == 1 && (m.w == KIND_ITEM || m.w == KIND_PREFIX)) continue;  // read in place (vmap)
     const bool rot = kv == 0 && (m.w == KIND_ITEM || m.w == KIND_HIST);
     float cc[8], ss[8];
     if (rot) {

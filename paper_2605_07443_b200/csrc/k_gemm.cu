@@ -327,6 +327,8 @@ __device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool ro
     uint16_t* dst;
     if (is_q) dst = ep.q_out + static_cast<int64_t>(row) * ep.q_ld + hh * DH;
     else if (is_k) dst = ep.arena_k + static_cast<int64_t>(hh - H) * ep.head_stride + static_cast<int64_t>(drow) * DH;
+    else if (DEV && ep.vsrc.vmap)  // zero-copy V: the stitched V row may live in a pool
+      dst = const_cast<uint16_t*>(vsrc_row(ep.vsrc, ep.arena_v, ep.head_stride, hh - H - Hk, drow, DH));
     else dst = ep.arena_v + static_cast<int64_t>(hh - H - Hk) * ep.head_stride + static_cast<int64_t>(drow) * DH;
 #pragma unroll
     for (int c = 0; c < DH; c += 2 * CW) {

@@ -309,8 +309,24 @@ __global__ void k_export_kv(const uint16_t* __restrict__ arena, int64_t arena_ro
   if (lane == 0) scales[t * planes + plane] = scale;
 }
 
+__global__ void k_scatter_i32(int32_t* __restrict__ dst, const int2* __restrict__ idx_val, int32_t n) {
+  griddep_wait();
+  griddep_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 e = idx_val[i];
+    dst[e.x] = e.y;
+  }
+}
+
+__global__ void k_vmap_identity(int32_t* __restrict__ vmap, const int32_t* __restrict__ rows, int32_t n) {
+  griddep_wait();
+  griddep_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) vmap[rows[i]] = rows[i];
+}
+
 __global__ void k_read_kv(const uint16_t* __restrict__ arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
-                          int32_t row0, int32_t n, uint16_t* __restrict__ k_out, uint16_t* __restrict__ v_out) {
+                          int32_t row0, int32_t n, uint16_t* __restrict__ k_out, uint16_t* __restrict__ v_out,
+                          const VSrc vs) {
   griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
   griddep_launch();
   const int64_t units = static_cast<int64_t>(2) * n * Hk * dh;
@@ -322,7 +338,9 @@ __global__ void k_read_kv(const uint16_t* __restrict__ arena, int64_t arena_rows
     r /= Hk;
     const int t = static_cast<int>(r % n);
     const int kv = static_cast<int>(r / n);
-    const uint16_t v = arena[(((static_cast<int64_t>(layer) * 2 + kv) * Hk + h) * arena_rows + row0 + t) * dh + j];
+    const uint16_t v = kv == 1 && vs.vmap
+        ? vsrc_row(vs, arena + (static_cast<int64_t>(layer) * 2 + 1) * Hk * arena_rows * dh, arena_rows * dh, h, row0 + t, dh)[j]
+        : arena[(((static_cast<int64_t>(layer) * 2 + kv) * Hk + h) * arena_rows + row0 + t) * dh + j];
     (kv == 0 ? k_out : v_out)[(static_cast<int64_t>(t) * Hk + h) * dh + j] = v;
   }
 }
@@ -429,10 +447,20 @@ cudaError_t export_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t 
                     dh, row0, n, int8, out, scales);
 }
 cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh, int32_t row0,
-                           int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s) {
+                           int32_t n, uint16_t* k_out, uint16_t* v_out, const VSrc& vs, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   return launch_pdl(k_read_kv, dim3(blocks_for(static_cast<int64_t>(2) * n * Hk * dh)), dim3(256), 0, s, arena, arena_rows, layer, Hk, dh, row0, n,
-                                                                             k_out, v_out);
+                                                                             k_out, v_out, vs);
+}
+cudaError_t scatter_i32_launch(int32_t* dst, const int2* idx_val, int32_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(k_scatter_i32, dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024))), dim3(256), 0,
+                    s, dst, idx_val, n);
+}
+cudaError_t vmap_identity_launch(int32_t* vmap, const int32_t* rows, int32_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(k_vmap_identity, dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024))), dim3(256), 0,
+                    s, vmap, rows, n);
 }
 
 }  // namespace rc

@@ -213,6 +213,10 @@ struct rc_ctx {
   // arena
   uint16_t* arena = nullptr;
   RangeAlloc arena_alloc;
+  // NEXT-4 zero-copy V (RC_ZERO_COPY_V=1): item / prefix V rows stay in their pools at the layers >= c;
+  // vmap[arena row] says where each stitched V row lives (rc_internal.h VSRC_*)
+  bool zc_v = false;
+  int32_t* vmap = nullptr;
   std::unordered_map<uint64_t, Seq> seqs;
   uint64_t next_seq = 1;
   // rope tables
@@ -281,7 +285,7 @@ struct rc_ctx {
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
                     a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
-                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt};
+                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt, vmap};
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
@@ -352,6 +356,19 @@ rc_status build_rope(rc_ctx* c) {
 }
 
 int64_t plane_count(const rc_ctx* c) { return static_cast<int64_t>(c->m.n_layers) * 2 * c->m.n_kv_heads; }
+
+// the V sources of layer l under zero-copy V (empty VSrc: every V row in the arena)
+VSrc layer_vsrc(const rc_ctx* c, int l) {
+  VSrc v;
+  if (!c->zc_v) return v;
+  const int64_t hk = c->m.n_kv_heads, dh = c->m.head_dim;
+  v.vmap = c->vmap;
+  v.item = c->item_pool ? c->item_pool + ((static_cast<int64_t>(l) * 2 + 1) * hk) * c->pd.item_rows * dh : nullptr;
+  v.item_head_stride = c->pd.item_rows * dh;
+  v.prefix = c->prefix_pool ? c->prefix_pool + ((static_cast<int64_t>(l) * 2 + 1) * hk) * c->pd.prefix_rows * dh : nullptr;
+  v.prefix_head_stride = c->pd.prefix_rows * dh;
+  return v;
+}
 
 // mark a resident item block used at the current clock (keeps the remote-region LRU index in sync)
 void touch(rc_ctx* c, uint64_t id, Block& b) {
@@ -533,6 +550,15 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   // masked, and 0 * finite = 0 inside P V)
   RC_CUDA(cudaMemset(c->arena, 0, static_cast<size_t>(planes) * std::max<int64_t>(pd->arena_rows, 1) * dh * 2));
   c->arena_alloc.init(pd->arena_rows);
+  {
+    const char* zc = std::getenv("RC_ZERO_COPY_V");
+    c->zc_v = zc && zc[0] == '1';
+    std::vector<int32_t> ident(std::max<int64_t>(pd->arena_rows, 1));
+    for (size_t i = 0; i < ident.size(); ++i) ident[i] = static_cast<int32_t>(i);
+    c->vmap = dev_alloc<int32_t>(ident.size(), &e);
+    if (e != cudaSuccess) return fail(RC_E_NOMEM, "vmap");
+    RC_CUDA(cudaMemcpy(c->vmap, ident.data(), ident.size() * 4, cudaMemcpyHostToDevice));
+  }
   rc_status st = build_rope(c.get());
   if (st != RC_OK) return st;
   // workspace
@@ -817,8 +843,23 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
   }
   for (size_t i = 0; i < meta_all.size(); ++i) meta_all[i].x += static_cast<int>(rows[meta_all_req[i]]);
   for (size_t i = 0; i < meta_pre.size(); ++i) meta_pre[i].x += static_cast<int>(rows[meta_pre_req[i]]);
+  // ---- zero-copy V: where each arena row's V lives at the layers >= c (identity unless ITEM / PREFIX)
+  std::vector<int2> vcodes;
+  if (c->zc_v) {
+    for (int r = 0; r < n_req; ++r)
+      for (int p = 0; p < built[r].n; ++p) vcodes.push_back(make_int2(static_cast<int>(rows[r] + p), static_cast<int>(rows[r] + p)));
+    std::vector<int64_t> base(n_req + 1, 0);
+    for (int r = 0; r < n_req; ++r) base[r + 1] = base[r] + built[r].n;
+    for (size_t i = 0; i < meta_all.size(); ++i) {
+      const int4& t = meta_all[i];
+      const int r = meta_all_req[i];
+      const int64_t pos = t.x - rows[r];
+      if (t.w == RC_TOK_ITEM) vcodes[base[r] + pos].y = static_cast<int>((VSRC_ITEM << 30) | static_cast<uint32_t>(t.y));
+      if (t.w == RC_TOK_PREFIX) vcodes[base[r] + pos].y = static_cast<int>((VSRC_PREFIX << 30) | static_cast<uint32_t>(t.y));
+    }
+  }
   // ---- metadata H2D + gather
-  const size_t bytes = (meta_all.size() + meta_pre.size()) * sizeof(int4);
+  const size_t bytes = (meta_all.size() + meta_pre.size()) * sizeof(int4) + vcodes.size() * sizeof(int2);
   if (bytes > 0) {
     cudaError_t e;
     const int slot = c->stage.acquire(bytes, &e);
@@ -829,8 +870,14 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     int4* hm = static_cast<int4*>(c->stage.host[slot]);
     std::copy(meta_all.begin(), meta_all.end(), hm);
     std::copy(meta_pre.begin(), meta_pre.end(), hm + meta_all.size());
+    int2* hv = reinterpret_cast<int2*>(hm + meta_all.size() + meta_pre.size());
+    std::copy(vcodes.begin(), vcodes.end(), hv);
     int4* dm = static_cast<int4*>(c->stage.dev[slot]);
     RC_CUDA(cudaMemcpyAsync(dm, hm, bytes, cudaMemcpyHostToDevice, s));
+    if (!vcodes.empty())
+      RC_LAUNCH(RC_K_SMALL, 0, vcodes.size() * 12.0, -1,
+                scatter_i32_launch(c->vmap, reinterpret_cast<const int2*>(dm + meta_all.size() + meta_pre.size()),
+                                   static_cast<int32_t>(vcodes.size()), s));
     GatherArgs g{};
     g.n_kv_heads = c->m.n_kv_heads;
     g.head_dim = c->m.head_dim;
@@ -847,10 +894,12 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     b_pre = meta_pre.size() * rows_per_tok * 2 * row_b;
     g.meta = dm; g.n_tok = static_cast<int32_t>(meta_all.size());
     g.layer_begin = gather_from; g.layer_end = c->m.n_layers;
+    g.skip_pool_v = c->zc_v ? 1 : 0;  // zero-copy V: item / prefix V read in place at the layers >= c
     if (g.n_tok > 0 && g.layer_end > g.layer_begin)
       RC_LAUNCH(RC_K_GATHER, 0, b_all * (g.layer_end - g.layer_begin), -1, gather_launch(g, c->num_sms, s));
     g.meta = dm + meta_all.size(); g.n_tok = static_cast<int32_t>(meta_pre.size());
     g.layer_begin = 0; g.layer_end = gather_from;
+    g.skip_pool_v = 0;  // layers < c attend over the arena (their U rows are recomputed there)
     if (g.n_tok > 0 && g.layer_end > g.layer_begin)
       RC_LAUNCH(RC_K_GATHER, 0, b_pre * (g.layer_end - g.layer_begin), -1, gather_launch(g, c->num_sms, s));
     // the slot's device half is read by the gathers: reusable once they are done (any stream)
@@ -943,7 +992,7 @@ namespace {
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
 rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
                     const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min,
-                    bool paired, double attn_flops, int attn_pending, int det, cudaStream_t s) {
+                    bool paired, double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
   const double R = rows, norm_b = R * d * 6.0;
@@ -964,6 +1013,7 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
   at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
   at.n_heads = H; at.n_kv_heads = Hk; at.head_dim = dh;
   at.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dh)));
+  if (zc_layer && c->attn_tc) at.vsrc = layer_vsrc(c, l);  // NEXT-4: item / prefix V read in place
   static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
   at.debug_mode = attn_debug;
   at.n_splits = n_splits;
@@ -1226,7 +1276,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   for (int l = 0; l < cL; ++l) {
     // the layers < c decide Sel: their residual sums are always order-fixed (reproducible selection)
     st = run_layer(c, l, c->x, &c->mC_x, U, D32(o_pos), D32(o_dst), d_ut, n_ut, split_u, smin_u, pair_u, attn_u, -1, 1,
-                   s);
+                   false, s);
     if (st != RC_OK) return st;
   }
   // ---- a3: check-layer KV projection with fused RoPE + deviation epilogue
@@ -1242,6 +1292,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     ev.rope_cos = c->rope_cos; ev.rope_sin = c->rope_sin; ev.rope_zero = c->rope_zero;
     ev.n_heads = m.n_heads; ev.n_kv_heads = m.n_kv_heads; ev.head_dim = m.head_dim;
     ev.dev_out = c->dev; ev.row_reuse = reinterpret_cast<const uint8_t*>(db + o_reuse);
+    ev.vsrc = layer_vsrc(c, cL);  // zero-copy V: the stitched V of items / prefix lives in the pools
     const double Nkv = 2.0 * m.n_kv_heads * m.head_dim;
     RC_LAUNCH(RC_K_GEMM, gemm_flops(U, Nkv, d), gemm_bytes(U, Nkv, d, 2), -1,
               gemm_launch(&c->mA_a, &c->mB_kv[cL], nullptr, U, 2 * m.n_kv_heads * m.head_dim, d, c->bn_kv, EPI_DEV, ev,
@@ -1265,12 +1316,14 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     RC_CUDA(cudaMemcpyAsync(c->sel_dst, fs + S, S * 4, cudaMemcpyDeviceToDevice, s));
     RC_CUDA(cudaMemcpyAsync(c->sel_urow, fs + 2 * S, S * 4, cudaMemcpyDeviceToDevice, s));
   }
+  if (c->zc_v)  // Sel rows get fresh K/V in the arena at the layers >= c
+    RC_LAUNCH(RC_K_SMALL, 0, S * 8.0, -1, vmap_identity_launch(c->vmap, c->sel_dst, S, s));
   RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(S) * d * 8.0, -1,
             gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
   // ---- a5-a7: selective layers c..L-1 on Sel
   for (int l = cL; l < L; ++l) {
     st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, smin_s, pair_s, 0.0, pend_idx,
-                   prm->deterministic ? 1 : 0, s);
+                   prm->deterministic ? 1 : 0, c->zc_v, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout
@@ -1319,7 +1372,8 @@ rc_status rc_seq_read_kv(rc_ctx* c, rc_seq seq, int32_t layer, void* k_out, void
   RC_LAUNCH(RC_K_SMALL, 0, 0, -1,
             read_kv_launch(c->arena, c->pd.arena_rows, layer, c->m.n_kv_heads, c->m.head_dim,
                            static_cast<int32_t>(it->second.arena_row), it->second.n, static_cast<uint16_t*>(k_out),
-                           static_cast<uint16_t*>(v_out), s));
+                           static_cast<uint16_t*>(v_out),
+                           layer >= it->second.gather_from ? layer_vsrc(c, layer) : VSrc{}, s));
   return RC_OK;
 }
 

@@ -33,6 +33,28 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// NEXT-4 zero-copy V ("maps logical prompt sequences to scattered physical
+// memory pages"): for the layers >= c, the V row a stitched-arena row resolves to. One int32 per arena
+// row: bits 30-31 = source (VSRC_ARENA / VSRC_ITEM / VSRC_PREFIX), bits 0-29 = the row in that source.
+enum : uint32_t { VSRC_ARENA = 0u, VSRC_ITEM = 1u, VSRC_PREFIX = 2u };
+constexpr uint32_t VMAP_ROW_MASK = (1u << 30) - 1u;
+struct VSrc {                    // where each source's V planes live (one layer)
+  const int32_t* vmap = nullptr; // [arena rows]; nullptr: every V row is in the arena (no zero-copy)
+  const uint16_t* item = nullptr;    // item pool V plane of head 0 of the layer
+  int64_t item_head_stride = 0;      // item_rows * dh
+  const uint16_t* prefix = nullptr;  // prefix pool V plane of head 0 of the layer
+  int64_t prefix_head_stride = 0;
+};
+__device__ __forceinline__ const uint16_t* vsrc_row(const VSrc& v, const uint16_t* arena_head0, int64_t arena_head_stride,
+                                                    int kvh, int64_t arena_row, int dh) {
+  const uint32_t code = v.vmap ? static_cast<uint32_t>(__ldg(v.vmap + arena_row)) : static_cast<uint32_t>(arena_row);
+  const int64_t row = code & VMAP_ROW_MASK;
+  switch (code >> 30) {
+    case VSRC_ITEM: return v.item + kvh * v.item_head_stride + row * dh;
+    case VSRC_PREFIX: return v.prefix + kvh * v.prefix_head_stride + row * dh;
+    default: return arena_head0 + kvh * arena_head_stride + row * dh;
+  }
+}
 // ---------------------------------------------------------------- dense GEMM (tcgen05, k_gemm.cu)
 // C[M][N] = A[M][K] * B[N][K]^T, A and B bf16 K-major, fp32 accumulation in TMEM; the epilogue
 // decides what happens to each fp32 accumulator row.
@@ -62,6 +84,7 @@ struct EpiArgs {
   int32_t n_heads = 0, n_kv_heads = 0, head_dim = 0;
   unsigned long long* dev_out = nullptr;  // [M]
   const uint8_t* row_reuse = nullptr;     // [M]
+  VSrc vsrc;                              // DEV: where the stitched V rows live (zero-copy V)
   // residual epilogues: workspace for partial tiles (split-K / stream-K) summed in K order by the
   // last-arriving CTA of a tile (bitwise-reproducible x); counters zero between launches
   float* ws = nullptr;      // gemm_ws_floats()
@@ -95,8 +118,43 @@ struct GatherArgs {
   const uint16_t* prefix_pool; int64_t prefix_rows;
   uint16_t* arena; int64_t arena_rows;
   const float* rope_cos; const float* rope_sin; int32_t rope_zero;
+  int32_t skip_pool_v = 0;  // NEXT-4 zero-copy V: ITEM / PREFIX V rows stay in their pools (not copied)
 };
 cudaError_t gather_launch(const GatherArgs& g, int num_sms, cudaStream_t s);
+
+#ifdef RC_COMMON_CUH  // device helpers of the kernel files (common.cuh included first)
+// Zero-copy V (NEXT-4): the 128 rows of one V tile (d_h = 128), each from the arena or a pool (vmap),
+// into the two [128 rows][64 bf16] SWIZZLE_128B halves (16 KB apart) the PV MMA reads. A warp
+// resolves 4 rows per lane, then every cp.async instruction moves two whole 256-byte rows (lanes
+// 0-15 / 16-31, 16 bytes each: coalesced); chunk c of a row lands at ((c ^ (row & 7)) << 4) of its
+// 128-byte half row, the TMA SW128 pattern; rows past the arena capacity are zero-filled like TMA
+// out-of-bounds boxes. Completion is signalled per lane by cp_async_mbar_arrive.
+__device__ __forceinline__ void v_rows_cp_async(uint8_t* tile, const VSrc& vs, const uint16_t* arena_v,
+                                                int64_t arena_head_stride, int64_t arena_row0, int kvh, int64_t t_cap) {
+  constexpr int DHV = 128;
+  constexpr uint32_t HALFB = 128 * 64 * 2;
+  const int lane = threadIdx.x & 31;
+  uint64_t src[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t ar = arena_row0 + lane + 32 * i;
+    src[i] = ar < t_cap ? reinterpret_cast<uint64_t>(vsrc_row(vs, arena_v, arena_head_stride, kvh, ar, DHV)) : 0ull;
+  }
+  const int c = lane & 15;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int row = 32 * i + 2 * k + (lane >> 4);
+      const uint64_t p = __shfl_sync(0xffffffffu, src[i], row & 31);
+      const uint16_t* s = p ? reinterpret_cast<const uint16_t*>(p) + c * 8 : arena_v;
+      cp_async16(tile + (c >> 3) * HALFB + row * 128 + (((c & 7) ^ (row & 7)) << 4), s, p != 0ull);
+    }
+  }
+}
+#endif
+cudaError_t vmap_identity_launch(int32_t* vmap, const int32_t* rows, int32_t n, cudaStream_t s);
+cudaError_t scatter_i32_launch(int32_t* dst, const int2* idx_val, int32_t n, cudaStream_t s);  // dst[x] = y
 
 // ---------------------------------------------------------------- attention (k_attn.cu)
 struct AttnArgs {
@@ -121,6 +179,7 @@ struct AttnArgs {
   int32_t split_min = 0;     // > 0 with n_splits = 2: adaptive split (tiles under split_min KV tiles unsplit)
   int32_t* split_flag = nullptr;  // [n_tiles / n_splits][Hk]: 1 = the tile was split (adaptive mode)
   int32_t* work_ctr = nullptr;    // paired kernel: {next work item, finished CTAs}, zero between launches
+  VSrc vsrc;                      // zero-copy V: V rows through vmap (cp.async loads) instead of TMA boxes
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);
@@ -206,6 +265,6 @@ cudaError_t copy_segments_launch(const CopySeg* segs, int32_t n_segs, int64_t to
 cudaError_t export_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t planes, int32_t dh, int32_t row0,
                              int32_t n, int32_t int8, void* out, float* scales, cudaStream_t s);
 cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t layer, int32_t Hk, int32_t dh,
-                           int32_t row0, int32_t n, uint16_t* k_out, uint16_t* v_out, cudaStream_t s);
+                           int32_t row0, int32_t n, uint16_t* k_out, uint16_t* v_out, const VSrc& vs, cudaStream_t s);
 
 }  // namespace rc

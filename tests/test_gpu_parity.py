@@ -426,6 +426,56 @@ def test_transposed_gemm_modes_match_oracle(mode, tmp_path):
         assert rel_l2(z["hidden"][off[r]:off[r + 1]], forced["x_sel"]) < TOL
 
 
+def _zc_run(attn_kernel, wl_name="mini-llama"):
+    """Selective prefill (deterministic residual sums) of a 2-request MINI batch, plus the stitched
+    last-layer KV read back (V resolved through the zero-copy map when it is on)."""
+    wl = rcgen.WORKLOADS[wl_name]
+    case = make_case(wl, n_req=2)
+    pools = oracle_pools(case)
+    G = _gpu()
+    n_tok = sum(l.n for l in layouts(case))
+    ctx, _ = G.make_ctx(case, pools, n_tok)
+    lays = G.gpu_layouts(ctx, case)
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=1)
+    n_cand = sum(len(l["cand_idtok"]) for l in lays)
+    out = ctx.selective_prefill(seqs, 1500, 1500, check_layer=1, hidden=True, n_cand=n_cand, attn_kernel=attn_kernel,
+                                deterministic=True)
+    torch.cuda.synchronize()
+    res = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
+    for l in (1, wl.shape.n_layers - 1):
+        k, v = ctx.read_kv(seqs[0], l, len(lays[0]["tokens"]))
+        res[f"k{l}"], res[f"v{l}"] = G.bits(k), G.bits(v)
+    ctx.release(seqs)
+    ctx.close()
+    return res
+
+
+def _zc_child(attn_kernel, wl_name, path):
+    res = _zc_run(attn_kernel, wl_name)
+    np.savez(path, **{k: np.asarray(v) for k, v in res.items()})
+
+
+@pytest.mark.parametrize("wl_name,attn_kernel", [("mini-llama", 1), ("mini-llama", 2), ("mini-qwen", 1)])
+def test_zero_copy_v_equals_stitched_copy(wl_name, attn_kernel, tmp_path):
+    """NEXT-4 zero-copy V (RC_ZERO_COPY_V=1, child process): item and prefix V rows are read in place
+    from their pools through the vmap (cp.async tile loads in the single-tile and paired attention,
+    the check-layer deviation through the same map) instead of being copied into the stitched arena.
+    The same bytes reach the same arithmetic, so with order-fixed residual sums the selection, logits
+    and hidden states equal the copy path's bit for bit, and the resolved stitched V equals O-ASM."""
+    import subprocess, sys, os
+    path = str(tmp_path / "zc.npz")
+    code = ("import sys; sys.path.insert(0, %r); from tests.test_gpu_parity import _zc_child; _zc_child(%d, %r, %r)"
+            % (os.getcwd(), attn_kernel, wl_name, path))
+    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, RC_ZERO_COPY_V="1"), timeout=600)
+    zc = np.load(path)
+    ref = _zc_run(attn_kernel, wl_name)
+    for k in ("sel_pos", "logits", "hidden", "cand_scores"):
+        assert np.array_equal(zc[k], ref[k]), k
+    wl = rcgen.WORKLOADS[wl_name]
+    for l in (1, wl.shape.n_layers - 1):
+        assert np.array_equal(zc[f"v{l}"], ref[f"v{l}"]) and np.array_equal(zc[f"k{l}"], ref[f"k{l}"]), l
+
+
 # ----------------------------------------------------------------------------- NEXT-1: attention mass
 @pytest.mark.parametrize("wl,c,lam", [(rcgen.MINI_L, 0, 0.5), (rcgen.MINI_L, 1, 0.5), (rcgen.MINI_Q, 1, 0.0),
                                       (rcgen.MINI_Q, 0, 0.25)])
