@@ -109,20 +109,38 @@ __device__ __forceinline__ unsigned long long sel_key(unsigned long long dev, in
   return (dev << 13) | static_cast<unsigned long long>(8191 - pos);  // R6: D desc, then pos asc
 }
 
+// Per request (one CTA): both classes' top-k by the unique R6 key in one 8-bit radix select (8
+// passes over the key bytes, high to low; a histogram of each class's still-matching keys per pass,
+// the digit that holds the k-th largest found with warp shuffles -- warp c scans class c's 256 bins
+// as 8 per lane, a suffix sum across lanes); then the selected / FORCED flags are compacted in
+// position order with a two-level warp-shuffle scan.
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
 __global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
   griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
   griddep_launch();
   __shared__ uint8_t flag[SEL_MAX_U];
   __shared__ uint8_t cls[SEL_MAX_U];
-  __shared__ int hist[256];
-  __shared__ int sh_digit, sh_krem, sh_members;
-  __shared__ int scan[SEL_THREADS];
+  __shared__ int hist[2][256];
+  __shared__ int sh_digit[2], sh_krem[2], sh_members[2];
+  __shared__ int wsum[SEL_THREADS / 32];
   const int4 rq = a.req[blockIdx.x];
   const int4 rq2 = a.req2[blockIdx.x];
   const int u_off = rq.x, u_cnt = rq.y, sel_off = rq.z, n = rq.w;
   const int P = n - u_cnt;
   const int window = rq2.w;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 2) sh_members[tid] = 0;
+  __syncthreads();
+  int mh = 0, mi = 0;
   for (int i = tid; i < u_cnt; i += SEL_THREADS) {
     const int pos = P + i;
     int c = a.ucls[u_off + i];
@@ -130,66 +148,78 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
     if (in_win) c = CLS_FORCED;
     cls[i] = static_cast<uint8_t>(c);
     flag[i] = (c == CLS_FORCED) ? 1 : 0;
+    mh += c == CLS_HIST;
+    mi += c == CLS_ITEM;
+  }
+  if (mh) atomicAdd(&sh_members[0], mh);
+  if (mi) atomicAdd(&sh_members[1], mi);
+  __syncthreads();
+  const int kk[2] = {rq2.x, rq2.y};
+  // a class needs the radix select only when its budget is positive and below its size
+  const bool act0 = kk[0] > 0 && kk[0] < sh_members[0], act1 = kk[1] > 0 && kk[1] < sh_members[1];
+  unsigned long long prefix[2] = {0ull, 0ull}, mask = 0ull;
+  if (tid < 2) sh_krem[tid] = kk[tid];
+  if (act0 || act1) {
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 512; i += SEL_THREADS) (&hist[0][0])[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < u_cnt; i += SEL_THREADS) {
+        const int c = cls[i] == CLS_HIST ? 0 : cls[i] == CLS_ITEM ? 1 : -1;
+        if (c < 0 || !(c == 0 ? act0 : act1)) continue;
+        const unsigned long long key = sel_key(a.dev[u_off + i], P + i);
+        if ((key & mask) == prefix[c]) atomicAdd(&hist[c][(key >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (warp < 2 && (warp == 0 ? act0 : act1)) {  // warp c: digit of class c's k-th largest key
+        // lane l owns bins 255 - 8l .. 248 - 8l (high digits on low lanes: a prefix scan = from the top)
+        int b[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { b[j] = hist[warp][255 - 8 * lane - j]; tot += b[j]; }
+        const int incl = warp_incl_scan(tot);
+        const int krem = sh_krem[warp];
+        const int excl = incl - tot;
+        const bool mine = excl < krem && incl >= krem;
+        if (mine) {
+          int cacc = excl, dgt = 0, kr = krem;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (cacc + b[j] >= krem) { dgt = 255 - 8 * lane - j; kr = krem - cacc; break; }
+            cacc += b[j];
+          }
+          sh_digit[warp] = dgt;
+          sh_krem[warp] = kr;
+        }
+      }
+      __syncthreads();
+      prefix[0] |= static_cast<unsigned long long>(sh_digit[0]) << shift;
+      prefix[1] |= static_cast<unsigned long long>(sh_digit[1]) << shift;
+      mask |= 255ull << shift;
+    }
+  }
+  // keys are unique: exactly k member keys are >= the k-th largest (prefix); a class whose budget
+  // covers it entirely takes every member, a zero budget none
+  for (int i = tid; i < u_cnt; i += SEL_THREADS) {
+    const int c = cls[i] == CLS_HIST ? 0 : cls[i] == CLS_ITEM ? 1 : -1;
+    if (c < 0 || kk[c] <= 0) continue;
+    const bool act = c == 0 ? act0 : act1;
+    if (!act || sel_key(a.dev[u_off + i], P + i) >= prefix[c]) flag[i] = 1;
   }
   __syncthreads();
-  for (int pass = 0; pass < 2; ++pass) {
-    const int want = pass == 0 ? CLS_HIST : CLS_ITEM;
-    const int k = pass == 0 ? rq2.x : rq2.y;
-    if (tid == 0) sh_members = 0;
-    __syncthreads();
-    int cnt = 0;
-    for (int i = tid; i < u_cnt; i += SEL_THREADS) cnt += (cls[i] == want);
-    atomicAdd(&sh_members, cnt);
-    __syncthreads();
-    const int members = sh_members;
-    if (k <= 0) continue;
-    unsigned long long thr = 0;
-    if (k < members) {
-      unsigned long long prefix = 0, mask = 0;
-      if (tid == 0) sh_krem = k;
-      for (int shift = 56; shift >= 0; shift -= 8) {
-        for (int i = tid; i < 256; i += SEL_THREADS) hist[i] = 0;
-        __syncthreads();
-        for (int i = tid; i < u_cnt; i += SEL_THREADS) {
-          if (cls[i] != want) continue;
-          const unsigned long long key = sel_key(a.dev[u_off + i], P + i);
-          if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
-        }
-        __syncthreads();
-        if (tid == 0) {
-          int c = 0, krem = sh_krem, dgt = 0;
-          for (int d = 255; d >= 0; --d) {
-            if (c + hist[d] >= krem) { dgt = d; krem -= c; break; }
-            c += hist[d];
-          }
-          sh_digit = dgt;
-          sh_krem = krem;
-        }
-        __syncthreads();
-        prefix |= static_cast<unsigned long long>(sh_digit) << shift;
-        mask |= 255ull << shift;
-        __syncthreads();
-      }
-      thr = prefix;  // keys are unique: exactly k member keys are >= the k-th largest
-    }
-    for (int i = tid; i < u_cnt; i += SEL_THREADS)
-      if (cls[i] == want && sel_key(a.dev[u_off + i], P + i) >= thr) flag[i] = 1;
-    __syncthreads();
-  }
-  // compaction in position order
+  // compaction in position order: contiguous runs per thread, two-level warp-shuffle scan
   const int per = (u_cnt + SEL_THREADS - 1) / SEL_THREADS;
   const int b = tid * per, e = min(u_cnt, b + per);
   int cnt = 0;
   for (int i = b; i < e; ++i) cnt += flag[i];
-  scan[tid] = cnt;
+  const int winc = warp_incl_scan(cnt);
+  if (lane == 31) wsum[warp] = winc;
   __syncthreads();
-  for (int o = 1; o < SEL_THREADS; o <<= 1) {
-    const int v = tid >= o ? scan[tid - o] : 0;
-    __syncthreads();
-    scan[tid] += v;
-    __syncthreads();
+  if (warp == 0) {
+    const int v = lane < SEL_THREADS / 32 ? wsum[lane] : 0;
+    const int inc = warp_incl_scan(v);
+    if (lane < SEL_THREADS / 32) wsum[lane] = inc - v;  // exclusive warp offsets
   }
-  int w = sel_off + scan[tid] - cnt;
+  __syncthreads();
+  int w = sel_off + wsum[warp] + winc - cnt;
   for (int i = b; i < e; ++i) {
     if (!flag[i]) continue;
     a.sel_pos[w] = P + i;
