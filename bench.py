@@ -226,6 +226,34 @@ def build_ours(wl, batch, n_batches, rank, device, world=1, gather=None, host_fr
                 shard=shard, fetch=fetch, host_fetch=host_fetch)
 
 
+def roofline_rows(kern, pk, pk_kind):
+    """Roofline fraction of every kernel class next to the dominant one (the same per-launch event
+    timings): tensor-bound classes against the sustained bf16 peak, HBM-bound ones against the
+    measured copy bandwidth, with their algorithmic work per launch."""
+    rows = []
+    for k, e in kern.items():
+        if "tflops" in e and k in ("gemm", "attention"):
+            rows.append({"kernel": k, "bound": "tensor", "achieved": e["tflops"], "peak": pk["bf16_tflops_sustained"],
+                         "unit": "TFLOP/s", "frac": e["tflops"] / pk["bf16_tflops_sustained"],
+                         "ms_per_step": e["ms_per_step"], "peak_source": f"{pk_kind} bf16_tflops_sustained"})
+        elif "gbs" in e:
+            rows.append({"kernel": k, "bound": "hbm", "achieved": e["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": e["gbs"] / pk["hbm_gbs"], "ms_per_step": e["ms_per_step"],
+                         "peak_source": f"{pk_kind} hbm_gbs"})
+    return rows
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def host_bytes(batch_layouts):
     return int(sum(l["tokens"].nbytes + l["cls"].nbytes + l["src_id"].nbytes + l["src_off"].nbytes +
                    l["cand_idtok"].nbytes for l in batch_layouts))
@@ -342,7 +370,7 @@ def oracle_sample(wl, W_dev, cat, protos, sys_tok, req, r_bp, c, n_layers_sample
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    return {"value": n / T, "unit": UNIT, "cores": int(cores), "kind": "oracle",
+    return {"value": n / T, "unit": UNIT, "cores": int(cores), "cpu_model": cpu_model(), "kind": "oracle",
             "sample": f"1 request of {wl.name} (n={n}), oracle numpy fp64 on layers 0..{Ls - 1} of {shape.n_layers} "
                       f"({t:.1f} s measured), extrapolated to {shape.n_layers} layers by the algorithmic FLOP ratio "
                       f"{F(shape.n_layers) / F(Ls):.2f}",
@@ -383,7 +411,7 @@ def run_reference(args, wl):
                       "check_layer": args.check_layer, "lambda": args.lam, "parallelism": "dp1",
                       "sample": "each step = one request of the batch (the oracle serves requests one at a time; "
                                 "tok/s is independent of the batch size)"},
-           "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -583,6 +611,7 @@ def run_ours(args, wl):
                         "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)",
                         "timing": "CUDA events around every launch on the launching stream, on a second pass "
                                   "over the same K steps (kept out of the timed pass)"},
+           "roofline_kernels": roofline_rows(kern, pk, pk_kind),
            "kernels": kern, "gpu_launches": int(launches), "clocks": cl,
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_bytes(batches[0]),
                    "d2h_bytes_per_step": int(pin_l.numel() * 4 + pin_c.numel() * 4)}}
@@ -608,7 +637,7 @@ def run_ours(args, wl):
         try:
             res["cpu_baseline"] = {k: v for k, v in oracle_sample(wl, env["W"], env["cat"], env["protos"], env["sys"],
                                                                  env["reqs"][0], r_bp, c).items()
-                                   if k in ("value", "unit", "cores", "kind", "sample")}
+                                   if k in ("value", "unit", "cores", "cpu_model", "kind", "sample")}
         except Exception as ex:  # reported, never silently replaced
             res["cpu_baseline"] = {"error": repr(ex)}
     print(json.dumps(res))

@@ -105,6 +105,12 @@ typedef struct rc_request {
   uint64_t prefix_id;        /* registered PREFIX block (ignored when P == 0)               */
   int32_t n_cand;            /* candidates, slot order                                      */
   const int32_t* cand_idtok; /* [n_cand] ID token of each candidate (its first token, R19)  */
+  const int32_t* hist_proto_dev; /* optional DEVICE int32 [number of HIST positions]: their prototype
+                                 ids in position order, e.g. straight from rc_semlib_match (NEXT-3,
+                                 PAPER.md:549) -- resolved to pool rows on the device, src_id of HIST
+                                 positions ignored; NULL = the host src_id. An id that is not a
+                                 registered prototype (< 2^31) leaves that position's stitched K/V
+                                 unwritten and counts in rc_device_error_count (check it) */
 } rc_request;
 
 /* A prompt as segments: system prompt, history tokens,
@@ -193,6 +199,9 @@ rc_status rc_pool_contains(rc_ctx* ctx, int32_t kind, int32_t n, const uint64_t*
  * Errors: INVALID (n > max_seq_len, bad classes), CAPACITY (arena full). */
 rc_status rc_assemble(rc_ctx* ctx, int32_t n_req, const rc_request* reqs, int32_t miss_policy, int32_t gather_from,
                       rc_seq* out_seqs, uint64_t* out_missing, int32_t* n_missing, rc_stream stream);
+
+/* Device-side input errors since creation (unresolvable device-fed prototype ids); synchronises. */
+int64_t rc_device_error_count(rc_ctx* ctx);
 
 /* |Sel| per request for the given parameters (host; fixed by the layout, R5). */
 rc_status rc_sel_count(rc_ctx* ctx, int32_t n_req, const rc_seq* seqs, const rc_prefill_params* prm,

@@ -43,7 +43,7 @@ class PoolDesc(C.Structure):
 
 class Request(C.Structure):
     _fields_ = [("n", C.c_int32), ("token_ids", I32P), ("cls", U8P), ("src_id", I64P), ("src_off", I32P),
-                ("prefix_id", C.c_uint64), ("n_cand", C.c_int32), ("cand_idtok", I32P)]
+                ("prefix_id", C.c_uint64), ("n_cand", C.c_int32), ("cand_idtok", I32P), ("hist_proto_dev", C.c_void_p)]
 
 
 class Prompt(C.Structure):
@@ -105,6 +105,7 @@ def lib():
             "rc_diag_gemm": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int32, P]),
             "rc_diag_gemm_add": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_int32, P]),
             "rc_launch_count": (C.c_int64, [P]),
+            "rc_device_error_count": (C.c_int64, [P]),
             "rc_place_items": (C.c_int32, [C.c_int32, I32P, C.c_int32, I64P, I32P, C.c_int32, C.c_int32, C.c_double,
                                            C.c_int32, I32P, I64P, I64P]),
             "rc_route": (C.c_int32, [C.c_int32, I64P, I32P, I64P, C.c_int32, C.c_int32, U8P, C.c_double, C.c_double,
@@ -136,5 +137,6 @@ EXPORTED = ["rc_create", "rc_destroy", "rc_last_error", "rc_abi_version", "rc_de
             "rc_selective_prefill", "rc_release", "rc_pool_export", "rc_peer_attach", "rc_fetch_remote",
             "rc_seq_read_kv", "rc_diag_deviation_select", "rc_diag_gemm", "rc_launch_count", "rc_profile_begin",
             "rc_profile_end", "rc_place_items", "rc_route", "rc_fetch_host", "rc_semlib_build", "rc_semlib_match",
-            "rc_pool_list", "rc_peer_directory", "rc_seq_export_kv", "rc_diag_gemm_add"]
+            "rc_pool_list", "rc_peer_directory", "rc_seq_export_kv", "rc_diag_gemm_add",
+            "rc_device_error_count"]
 KINDS = ["gemm", "attention", "gather", "select", "small", "lm_head", "fetch"]

@@ -117,9 +117,10 @@ class RcContext:
                     np.ascontiguousarray(lay["src_id"], np.int64), np.ascontiguousarray(lay["src_off"], np.int32),
                     np.ascontiguousarray(lay["cand_idtok"], np.int32)]
             keep.append(arrs)
+            hp = lay.get("hist_proto_dev")  # optional CUDA int32 tensor (NEXT-3 device-fed prototypes)
             reqs[i] = R.Request(len(arrs[0]), np_ptr(arrs[0], C.c_int32), np_ptr(arrs[1], C.c_uint8),
                                 np_ptr(arrs[2], C.c_int64), np_ptr(arrs[3], C.c_int32), prefix_id, len(arrs[4]),
-                                np_ptr(arrs[4], C.c_int32))
+                                np_ptr(arrs[4], C.c_int32), hp.data_ptr() if hp is not None else None)
         seqs = np.zeros(n, np.uint64)
         missing = np.zeros(4096, np.uint64)
         nm = C.c_int32(len(missing))
@@ -204,6 +205,9 @@ class RcContext:
     def release(self, seqs):
         seqs = np.ascontiguousarray(seqs, np.uint64)
         lib().rc_release(self.ctx, len(seqs), np_ptr(seqs, C.c_uint64))
+
+    def device_error_count(self):
+        return int(lib().rc_device_error_count(self.ctx))
 
     def launch_count(self):
         return int(lib().rc_launch_count(self.ctx))

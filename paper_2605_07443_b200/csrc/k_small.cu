@@ -339,6 +339,28 @@ __global__ void k_export_kv(const uint16_t* __restrict__ arena, int64_t arena_ro
   if (lane == 0) scales[t * planes + plane] = scale;
 }
 
+__global__ void k_resolve_hist(int4* __restrict__ meta, int32_t n, const uint64_t* __restrict__ req_ptr,
+                               const int2* __restrict__ tab, int64_t cap, unsigned long long* err) {
+  griddep_wait();
+  griddep_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int4 m = meta[i];
+    if (m.w != RC_TOK_HIST_DEV) continue;
+    const int32_t* ids = reinterpret_cast<const int32_t*>(req_ptr[m.y >> 16]);
+    const int id = ids[m.y & 0xFFFF];
+    const int2 t = (id >= 0 && id < cap) ? tab[id] : make_int2(-1, 0);
+    if (t.x < 0) {  // not a registered prototype: counted, and the gather leaves the row unwritten
+      atomicAdd(err, 1ull);
+      m.w = CLS_FORCED;
+    } else {
+      m.y = t.x;
+      m.z = m.z - t.y;  // Delta = position - canonical position
+      m.w = CLS_HIST;
+    }
+    meta[i] = m;
+  }
+}
+
 __global__ void k_scatter_i32(int32_t* __restrict__ dst, const int2* __restrict__ idx_val, int32_t n) {
   griddep_wait();
   griddep_launch();
@@ -481,6 +503,12 @@ cudaError_t read_kv_launch(const uint16_t* arena, int64_t arena_rows, int32_t la
   if (n <= 0) return cudaSuccess;
   return launch_pdl(k_read_kv, dim3(blocks_for(static_cast<int64_t>(2) * n * Hk * dh)), dim3(256), 0, s, arena, arena_rows, layer, Hk, dh, row0, n,
                                                                              k_out, v_out, vs);
+}
+cudaError_t resolve_hist_launch(int4* meta, int32_t n, const uint64_t* req_ptr, const int2* proto_tab, int64_t tab_cap,
+                                unsigned long long* err, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(k_resolve_hist, dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024))), dim3(256), 0,
+                    s, meta, n, req_ptr, proto_tab, tab_cap, err);
 }
 cudaError_t scatter_i32_launch(int32_t* dst, const int2* idx_val, int32_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;

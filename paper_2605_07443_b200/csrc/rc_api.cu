@@ -198,6 +198,11 @@ struct rc_ctx {
   RangeAlloc item_alloc, remote_alloc;
   int64_t hist_used = 0, prefix_used = 0;
   std::unordered_map<uint64_t, Block> items, protos, prefixes;
+  // NEXT-3 device-fed prototypes: dense id -> {pool row, canonical position} (row -1 = unregistered)
+  std::vector<int2> proto_tab_host;
+  int2* proto_tab = nullptr;
+  int64_t proto_tab_cap = 0;
+  unsigned long long* dev_err = nullptr;  // device-side input errors (rc_device_error_count)
   // NEXT-2 host tier: pinned, mapped host DRAM in the pool layout [L][2][Hk][host_rows][dh]
   uint16_t* host_pool = nullptr;      // host pointer
   uint16_t* host_pool_dev = nullptr;  // its device mapping (registration writes)
@@ -285,7 +290,7 @@ struct rc_ctx {
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
                     a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
-                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt, vmap};
+                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt, vmap, proto_tab, dev_err};
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
@@ -433,6 +438,13 @@ extern "C" {
 const char* rc_last_error(void) { return g_err.c_str(); }
 int32_t rc_abi_version(void) { return 1; }
 int64_t rc_launch_count(rc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t rc_device_error_count(rc_ctx* ctx) {
+  if (!ctx || !ctx->dev_err) return 0;
+  unsigned long long v = 0;
+  if (cudaSetDevice(ctx->device) != cudaSuccess ||
+      cudaMemcpy(&v, ctx->dev_err, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return static_cast<int64_t>(v);
+}
 
 rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_desc* pd, int32_t device, rc_ctx** out) {
   if (!md || !w || !pd || !out) return fail(RC_E_INVALID, "null argument");
@@ -559,6 +571,9 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
     if (e != cudaSuccess) return fail(RC_E_NOMEM, "vmap");
     RC_CUDA(cudaMemcpy(c->vmap, ident.data(), ident.size() * 4, cudaMemcpyHostToDevice));
   }
+  c->dev_err = dev_alloc<unsigned long long>(1, &e);
+  if (e != cudaSuccess) return fail(RC_E_NOMEM, "device error counter");
+  RC_CUDA(cudaMemset(c->dev_err, 0, sizeof(unsigned long long)));
   rc_status st = build_rope(c.get());
   if (st != RC_OK) return st;
   // workspace
@@ -727,7 +742,28 @@ rc_status rc_pool_register_blocks(rc_ctx* c, int32_t kind, int32_t n_blocks, con
     (*dir)[ids[i]] = Block{r, n_tokens[i], canon_pos[i], false, 0};
     r += n_tokens[i];
   }
-  if (kind == RC_POOL_HIST_INT8) c->hist_used += total;
+  if (kind == RC_POOL_HIST_INT8) {
+    c->hist_used += total;
+    // the dense device table of prototype ids < 2^31 (device-fed rc_assemble, NEXT-3)
+    int64_t need = c->proto_tab_cap;
+    for (int i = 0; i < n_blocks; ++i)
+      if (ids[i] < (1ull << 31)) need = std::max<int64_t>(need, static_cast<int64_t>(ids[i]) + 1);
+    if (static_cast<int64_t>(c->proto_tab_host.size()) < need) c->proto_tab_host.resize(need, make_int2(-1, 0));
+    for (int i = 0; i < n_blocks; ++i)
+      if (ids[i] < (1ull << 31)) {
+        const Block& b = c->protos[ids[i]];
+        c->proto_tab_host[ids[i]] = make_int2(static_cast<int>(b.row), b.canon);
+      }
+    if (need > c->proto_tab_cap) {
+      if (c->proto_tab) cudaFree(c->proto_tab);
+      cudaError_t e2;
+      c->proto_tab = dev_alloc<int2>(need, &e2);
+      if (e2 != cudaSuccess) { c->proto_tab = nullptr; c->proto_tab_cap = 0; return fail(RC_E_NOMEM, "prototype table"); }
+      c->proto_tab_cap = need;
+    }
+    if (need > 0)
+      RC_CUDA(cudaMemcpyAsync(c->proto_tab, c->proto_tab_host.data(), need * sizeof(int2), cudaMemcpyHostToDevice, s));
+  }
   if (kind == RC_POOL_PREFIX_BF16) c->prefix_used += total;
   if (kind == RC_POOL_ITEM_HOST_BF16) c->host_used += total;
   return RC_OK;
@@ -764,6 +800,10 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
   std::vector<uint64_t> missing;
   std::vector<int4> meta_all, meta_pre;  // {dst_row(rel), src_row, delta, kind}; dst fixed up after alloc
   std::vector<int> meta_all_req, meta_pre_req;
+  std::vector<int> n_hist_dev(n_req, 0);  // device-fed HIST tokens per request
+  bool any_dev = false;
+  for (int r = 0; r < n_req; ++r) any_dev |= reqs[r].hist_proto_dev != nullptr;
+  if (any_dev && !c->proto_tab) return fail(RC_E_NOTFOUND, "device-fed prototypes but no prototype registered");
   for (int r = 0; r < n_req; ++r) {
     const rc_request& q = reqs[r];
     if (q.n <= 0 || q.n > c->pd.max_seq_len) return fail(RC_E_INVALID, "request length out of range");
@@ -795,6 +835,12 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
         meta_all_req.push_back(r);
         if (gather_from > 0) { meta_pre.push_back(meta_all.back()); meta_pre_req.push_back(r); }
       } else if (k == RC_TOK_HIST) {
+        if (q.hist_proto_dev) {  // resolved on the device (k_resolve_hist): y = (request, HIST index), z = position
+          if (r >= (1 << 15) || n_hist_dev[r] >= (1 << 16)) return fail(RC_E_INVALID, "device-fed history too large");
+          meta_all.push_back(make_int4(p, (r << 16) | n_hist_dev[r]++, p, RC_TOK_HIST_DEV));
+          meta_all_req.push_back(r);
+          continue;
+        }
         auto it = c->protos.find(static_cast<uint64_t>(q.src_id[p]));
         if (it == c->protos.end()) return fail(RC_E_NOTFOUND, "prototype not registered: " + std::to_string(q.src_id[p]));
         meta_all.push_back(make_int4(p, static_cast<int>(it->second.row), p - it->second.canon, RC_TOK_HIST));
@@ -859,7 +905,8 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     }
   }
   // ---- metadata H2D + gather
-  const size_t bytes = (meta_all.size() + meta_pre.size()) * sizeof(int4) + vcodes.size() * sizeof(int2);
+  const size_t bytes = (meta_all.size() + meta_pre.size()) * sizeof(int4) + vcodes.size() * sizeof(int2) +
+                       (any_dev ? n_req * sizeof(uint64_t) : 0);
   if (bytes > 0) {
     cudaError_t e;
     const int slot = c->stage.acquire(bytes, &e);
@@ -872,8 +919,16 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     std::copy(meta_pre.begin(), meta_pre.end(), hm + meta_all.size());
     int2* hv = reinterpret_cast<int2*>(hm + meta_all.size() + meta_pre.size());
     std::copy(vcodes.begin(), vcodes.end(), hv);
+    uint64_t* hp = reinterpret_cast<uint64_t*>(hv + vcodes.size());
+    if (any_dev)
+      for (int r = 0; r < n_req; ++r) hp[r] = reinterpret_cast<uint64_t>(reqs[r].hist_proto_dev);
     int4* dm = static_cast<int4*>(c->stage.dev[slot]);
     RC_CUDA(cudaMemcpyAsync(dm, hm, bytes, cudaMemcpyHostToDevice, s));
+    if (any_dev)  // NEXT-3: prototype ids produced on the device -> pool rows and Delta, before the gather
+      RC_LAUNCH(RC_K_SMALL, 0, meta_all.size() * 16.0, -1,
+                resolve_hist_launch(dm, static_cast<int32_t>(meta_all.size()),
+                                    reinterpret_cast<const uint64_t*>(reinterpret_cast<int2*>(dm + meta_all.size() + meta_pre.size()) + vcodes.size()),
+                                    c->proto_tab, c->proto_tab_cap, c->dev_err, s));
     if (!vcodes.empty())
       RC_LAUNCH(RC_K_SMALL, 0, vcodes.size() * 12.0, -1,
                 scatter_i32_launch(c->vmap, reinterpret_cast<const int2*>(dm + meta_all.size() + meta_pre.size()),
@@ -890,7 +945,8 @@ rc_status rc_assemble(rc_ctx* c, int32_t n_req, const rc_request* reqs, int32_t 
     // written once (bf16 rows 2*dh bytes; int8 rows dh bytes + one fp32 scale)
     const double row_b = 2.0 * c->m.head_dim, rows_per_tok = 2.0 * c->m.n_kv_heads;
     double b_all = 0, b_pre = 0;
-    for (auto& t : meta_all) b_all += rows_per_tok * (t.w == RC_TOK_HIST ? (c->m.head_dim + 4.0 + row_b) : 2 * row_b);
+    for (auto& t : meta_all)
+      b_all += rows_per_tok * (t.w == RC_TOK_HIST || t.w == RC_TOK_HIST_DEV ? (c->m.head_dim + 4.0 + row_b) : 2 * row_b);
     b_pre = meta_pre.size() * rows_per_tok * 2 * row_b;
     g.meta = dm; g.n_tok = static_cast<int32_t>(meta_all.size());
     g.layer_begin = gather_from; g.layer_end = c->m.n_layers;

@@ -121,6 +121,11 @@ struct GatherArgs {
   int32_t skip_pool_v = 0;  // NEXT-4 zero-copy V: ITEM / PREFIX V rows stay in their pools (not copied)
 };
 cudaError_t gather_launch(const GatherArgs& g, int num_sms, cudaStream_t s);
+// NEXT-3 device-fed prototypes: meta entries of kind RC_TOK_HIST_DEV {dst, (request << 16) | j, pos, 4}
+// -> {dst, pool row, pos - canon, RC_TOK_HIST} from proto ids req_ptr[request][j] and the dense table
+enum { RC_TOK_HIST_DEV = 4 };
+cudaError_t resolve_hist_launch(int4* meta, int32_t n, const uint64_t* req_ptr, const int2* proto_tab, int64_t tab_cap,
+                                unsigned long long* err, cudaStream_t s);
 
 #ifdef RC_COMMON_CUH  // device helpers of the kernel files (common.cuh included first)
 // Zero-copy V (NEXT-4): the 128 rows of one V tile (d_h = 128), each from the arena or a pool (vmap),

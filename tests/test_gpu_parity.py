@@ -5,6 +5,8 @@ hidden states x_L[Sel], last-token logits and KV_st[L-1][Sel] within relative L2
 identical candidate ranking where the oracle's adjacent top-11 gaps exceed 4x the measured
 logit error (R19).
 """
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -558,4 +560,49 @@ def test_semlib_match_bitexact(wl, n_req):
         assert pid[i] == p and np.float32(c).view(np.uint32) == cos[i].view(np.uint32), (i, pid[i], p, cos[i], c)
     # the generator's exact-match tokens (93%) find a prototype with their own embedding (cosine 1)
     assert (np.abs(cos[:-33] - 1.0) < 1e-6).mean() > 0.5
+    ctx.close()
+
+
+def test_semlib_feeds_assemble_on_device():
+    """NEXT-3 end to end on the device: the history tokens' prototype ids
+    come straight from rc_semlib_match (device memory) into rc_assemble (rc_request.hist_proto_dev),
+    resolved to pool rows and Delta on the device; the stitched KV equals O-ASM of the layout whose
+    history tokens carry the oracle's own LSH matches (oracle/semlib.py), bit for bit."""
+    from oracle.semlib import Library, T, B, D
+    from oracle.layout import layout_from_request
+    G = _gpu()
+    wl = rcgen.MINI_L
+    case = make_case(wl, n_req=2)
+    shape, protos = case["shape"], case["protos"]
+    pools = oracle_pools(case)
+    all_ids = list(range(protos.n))            # every prototype registered, block id = library index
+    hq, hs = rcgen.pools.hist_kv(shape, all_ids)
+    pools.update(proto_ids=all_ids, hist_q=hq, hist_s=hs,
+                 hist={pi: (hq[j].numpy(), hs[j].numpy(), int(protos.canon_pos[pi])) for j, pi in enumerate(all_ids)})
+    n_tok = sum(l.n for l in layouts(case))
+    ctx, _ = G.make_ctx(case, pools, n_tok)
+    H = np.random.default_rng(9).standard_normal((T * B, D)).astype(np.float32)
+    offs = (protos.canon_pos - wl.prefix_len).astype(np.int32)
+    ctx.semlib_build(protos.token, offs, protos.n_buckets, H, seed=3)
+    lib = Library(protos.token, offs, protos.n_buckets, H, 3)
+    lays = G.gpu_layouts(ctx, case)
+    for r, req in enumerate(case["reqs"]):
+        tok = torch.from_numpy(np.ascontiguousarray(req.hist_tokens, np.int32)).cuda()
+        off = torch.arange(len(req.hist_tokens), dtype=torch.int32, device="cuda")
+        pid, _ = ctx.semlib_match(tok, off)
+        lays[r]["hist_proto_dev"] = pid           # device ids, never copied to the host
+        lays[r]["src_id"] = np.where(lays[r]["cls"] == HIST, -1, lays[r]["src_id"])  # host ids ignored
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=1)
+    torch.cuda.synchronize()
+    assert ctx.device_error_count() == 0
+    for r, req in enumerate(case["reqs"]):
+        matched = [lib.match(int(t), j)[0] for j, t in enumerate(req.hist_tokens)]
+        lay = layout_from_request(dataclasses.replace(req, hist_protos=np.array(matched, np.int64)), case["cat"],
+                                  case["sys"])
+        K, V, dfn = assemble(shape, lay, pools["items"], pools["hist"], pools["prefix"], 1)
+        for l in range(1, shape.n_layers):
+            k, v = ctx.read_kv(seqs[r], l, lay.n)
+            m = dfn[l]
+            assert np.array_equal(G.bits(k)[m], K[l][m]) and np.array_equal(G.bits(v)[m], V[l][m]), (r, l)
+    ctx.release(seqs)
     ctx.close()
