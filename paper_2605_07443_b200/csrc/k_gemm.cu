@@ -1042,7 +1042,8 @@ cudaError_t launch_t(const CUtensorMap* w, const CUtensorMap* x128, const CUtens
   const int ntt = (M + 255) / 256;
   const int tiles = (N / 256) * ntt;
   const int nk = (K + BK - 1) / BK;
-  const int splits = EPI == EPI_ADD_F32 ? choose_splits(tiles, nk, pairs, ep) : 1;
+  static const int max_splits = [] { const char* e = std::getenv("RC_GEMM_T_SPLITS"); return e ? std::atoi(e) : 16; }();
+  const int splits = EPI == EPI_ADD_F32 ? std::min(max_splits, choose_splits(tiles, nk, pairs, ep)) : 1;
   const int units = tiles * splits;
   const int grid = 2 * (units < pairs ? units : pairs);
   return launch_pdl(k_gemm_t<EPI>, dim3(grid), dim3(256), C::SMEM, s, *w, *x128, *x64, c ? *c : *w, M, N, K, splits,
