@@ -83,19 +83,32 @@ def select_heavy_hitters(scores, r_bp, window, n):
     return sorted(set(top) | set(win))
 
 
-def select_sel(cls, D, r_rev_bp, r_item_bp, window=0):
+def select_sel(cls, D, r_rev_bp, r_item_bp, window=0, among=None):
     """Sel for one request: FORCED u window u topk(HIST) u topk(ITEM), sorted by position.
-    D: per-position integer deviation (only HIST/ITEM entries are read)."""
+    D: per-position integer deviation (only HIST/ITEM entries are read).
+    among (gradual filtering, reading R-GF): the previous step's Sel; the top-k of a class is taken
+    over its positions in `among` only, with the budget still ceil(r * |class|) over the whole class."""
     n = len(cls)
     win = set(range(max(0, n - window), n)) if window > 0 else set()
     win = {p for p in win if cls[p] != PREFIX}
     sel = {p for p in range(n) if cls[p] == FORCED} | win
     D = [int(d) for d in D]
+    pool = None if among is None else {int(p) for p in among}
     for c, r_bp in ((HIST, r_rev_bp), (ITEM, r_item_bp)):
         members = [p for p in range(n) if cls[p] == c and p not in win]
         k = budget(r_bp, len(members))
-        sel |= set(topk_order(D, members)[:k])
+        cand = members if pool is None else [p for p in members if p in pool]
+        assert k <= len(cand), "a gradual step cannot grow a class"
+        sel |= set(topk_order(D, cand)[:k])
     return np.array(sorted(sel), dtype=np.int32)
+
+
+def gradual_ratio_bp(r_start_bp, r_bp, i, g):
+    """Reading R-GF: the ratio of gradual step i in [0, g], linear from r_start (check layer c) to r
+    (layer c + g), truncated: r_start - floor((r_start - r) * i / g)."""
+    if g == 0:
+        return int(r_bp)
+    return int(r_start_bp) - (int(r_start_bp) - int(r_bp)) * int(i) // int(g)
 
 
 def sel_count(cls, r_rev_bp, r_item_bp, window=0):
