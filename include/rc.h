@@ -151,7 +151,23 @@ typedef struct rc_prefill_params {
                                  1 = the layers >= c as well (logits and hidden states bitwise
                                  reproducible, at the cost of a workspace round trip per split
                                  tile); 0 = those partials meet in fp32 reduce-adds in arrival order */
+  /* Gradual filtering (NEXT-1 variant, reading R-GF; the CacheBlend scheme PAPER.md:557
+     cites for "token importance persists across layers"). gradual_layers = g in [0, RC_MAX_GRADUAL]
+     (0 = the one-shot selection above; zero-initialised fields keep it off): Sel_0 is taken at the
+     check layer with the ratios r_start_*_bp (r_*_bp <= r_start_*_bp <= 10000); each layer
+     l = c + i, i = 1..g, computes q/k/v for the rows of Sel_{i-1}, scores their HIST/ITEM rows by
+     the Eq. 3 divergence (R4 fixed point) of that layer's fresh K/V against the stitched K/V, stores
+     the fresh K/V of all of Sel_{i-1}, and keeps Sel_i = FORCED u window u per-class top-k_i among
+     Sel_{i-1} at ratio r_i = r_start - floor((r_start - r) i / g); its attention and MLP run on
+     Sel_i. Needs c + g <= L - 1; not with forced_sel or RC_ZERO_COPY_V (UNSUPPORTED). rc_sel_count
+     and sel_pos_out / hidden refer to the final Sel_g. */
+  int32_t gradual_layers;
+  int32_t r_start_rev_bp, r_start_item_bp;
+  int32_t* sel_trace;         /* optional device [sum_i |Sel_i|]: the positions of Sel_0 .. Sel_g,
+                                 step-major, request-major within a step, ascending (each step's
+                                 sizes: rc_sel_count at r_i); NULL = none */
 } rc_prefill_params;
+enum { RC_MAX_GRADUAL = 16 };
 enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3, RC_ATTN_ADAPTIVE = 4 };
 /* RC_ATTN_SPLIT2: every query tile's KV range in two CTAs + merge; RC_ATTN_ADAPTIVE: the same launch,
    but tiles shorter than half the longest prompt's KV run unsplit (decided on the device from the

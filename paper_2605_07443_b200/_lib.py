@@ -58,7 +58,9 @@ RC_ATTN_AUTO, RC_ATTN_SINGLE, RC_ATTN_PAIRED, RC_ATTN_SPLIT2, RC_ATTN_ADAPTIVE =
 class PrefillParams(C.Structure):
     _fields_ = [("r_rev_bp", C.c_int32), ("r_item_bp", C.c_int32), ("lambda_", C.c_float),
                 ("check_layer", C.c_int32), ("window", C.c_int32), ("forced_sel", I32P), ("forced_sel_off", I32P),
-                ("attn_kernel", C.c_int32), ("score_out", C.c_void_p), ("deterministic", C.c_int32)]
+                ("attn_kernel", C.c_int32), ("score_out", C.c_void_p), ("deterministic", C.c_int32),
+                ("gradual_layers", C.c_int32), ("r_start_rev_bp", C.c_int32), ("r_start_item_bp", C.c_int32),
+                ("sel_trace", C.c_void_p)]
 
 
 _LIB = None

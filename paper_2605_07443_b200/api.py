@@ -130,9 +130,12 @@ class RcContext:
         check(code)
         return seqs
 
-    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0, attn_kernel=0, deterministic=0):
+    def _params(self, r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam=1.0, attn_kernel=0, deterministic=0,
+                gradual=0, r_start_rev_bp=None, r_start_item_bp=None):
         prm = R.PrefillParams(r_rev_bp, r_item_bp, lam, check_layer, window, None, None, attn_kernel, None,
-                              int(deterministic))
+                              int(deterministic), int(gradual),
+                              int(r_rev_bp if r_start_rev_bp is None else r_start_rev_bp),
+                              int(r_item_bp if r_start_item_bp is None else r_start_item_bp), None)
         keep = None
         if forced_sel is not None:
             off = np.zeros(len(forced_sel) + 1, np.int32)
@@ -152,17 +155,35 @@ class RcContext:
 
     def selective_prefill(self, seqs, r_rev_bp, r_item_bp, check_layer=1, window=0, forced_sel=None, lam=1.0,
                           logits=True, cand_scores=True, sel_pos=True, hidden=False, n_cand=None, out=None,
-                          stream=None, attn_kernel=0, score_out=None, deterministic=False):
+                          stream=None, attn_kernel=0, score_out=None, deterministic=False, gradual=0,
+                          r_start_rev_bp=None, r_start_item_bp=None, sel_trace=False):
         """Returns dict of CUDA tensors (logits, cand_scores, sel_pos, hidden) as requested. `out`
         may hold preallocated tensors with the same keys (reused; no allocation). score_out: optional
         int64 CUDA tensor [sum |U|] receiving the selection score of every U row (lam < 1: Eq. 3
-        with the attention-mass term, NEXT-1)."""
+        with the attention-mass term, NEXT-1). gradual > 0: gradual filtering from the r_start
+        ratios at the check layer down to r at layer c + gradual (reading R-GF); sel_trace=True
+        adds "sel_trace" (the positions of Sel_0 .. Sel_g, step-major) and "trace_off" (per step
+        and request, offsets into it)."""
         seqs = np.ascontiguousarray(seqs, np.uint64)
-        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam, attn_kernel, deterministic)
+        prm, keep = self._params(r_rev_bp, r_item_bp, check_layer, window, forced_sel, lam, attn_kernel, deterministic,
+                                 gradual, r_start_rev_bp, r_start_item_bp)
         if score_out is not None:
             prm.score_out = score_out.data_ptr()
-        dev = torch.device("cuda", self.device)
         res = dict(out) if out else {}
+        if sel_trace and "sel_trace" not in res:
+            rh0 = r_rev_bp if r_start_rev_bp is None else r_start_rev_bp
+            ri0 = r_item_bp if r_start_item_bp is None else r_start_item_bp
+            sizes = []
+            for i in range(int(gradual) + 1):   # rc.h: r_i = r_start - floor((r_start - r) i / g)
+                rh = rh0 - (rh0 - r_rev_bp) * i // gradual if gradual else r_rev_bp
+                ri = ri0 - (ri0 - r_item_bp) * i // gradual if gradual else r_item_bp
+                sizes.append(self.sel_count(seqs, rh, ri, check_layer, window))
+            sizes = np.stack(sizes)
+            res["trace_off"] = np.concatenate([[0], np.cumsum(sizes.ravel())]).astype(np.int64)
+            res["sel_trace"] = torch.empty((int(sizes.sum()),), dtype=torch.int32, device=torch.device("cuda", self.device))
+        if "sel_trace" in res:
+            prm.sel_trace = res["sel_trace"].data_ptr()
+        dev = torch.device("cuda", self.device)
         if (sel_pos or hidden) and ("sel_pos" not in res and "hidden" not in res):
             cnt = self.sel_count(seqs, r_rev_bp, r_item_bp, check_layer, window)
             S = int(cnt.sum())

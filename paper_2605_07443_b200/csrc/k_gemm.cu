@@ -307,10 +307,13 @@ __device__ __forceinline__ void rope_row_load(RopeRow<DH>& rr, int row, bool row
 }
 
 // Fused QKV / deviation epilogue over the heads of one tile. Columns of a head come in rotate-half
-// pairs: column 2i = dim i, 2i + 1 = dim i + DH/2 (packed layout).
-template <int BN, int DH, bool DEV>
+// pairs: column 2i = dim i, 2i + 1 = dim i + DH/2 (packed layout). MODE 0: QKV (store q, k, v);
+// 1: DEV (k, v only, score against the stitched rows, no store); 2: QKV_DEV (score k, v against the
+// stitched rows, then overwrite them; `score` = this row's k/v are scored).
+template <int BN, int DH, int MODE>
 __device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool row_ok, int row, const EpiArgs& ep,
-                                          const RopeRow<DH>& rr, unsigned long long& dev_acc) {
+                                          const RopeRow<DH>& rr, unsigned long long& dev_acc, bool score) {
+  constexpr bool DEV = MODE == 1;
   constexpr int CW = DH >= 32 ? 16 : 8;  // dims per chunk and half: 2 CW accumulator columns
   const int H = DEV ? 0 : ep.n_heads;
   const int Hk = ep.n_kv_heads;
@@ -360,6 +363,14 @@ __device__ __forceinline__ void epi_heads(uint32_t taddr, int n0, int N, bool ro
           dev_acc += dev_term(y1[j], dst[DH / 2 + i0 + j]);
         }
       } else {
+        if constexpr (MODE == 2) {
+          if (!is_q && score)  // the stitched value is read before this thread overwrites it
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+              dev_acc += dev_term(y0[j], dst[i0 + j]);
+              dev_acc += dev_term(y1[j], dst[DH / 2 + i0 + j]);
+            }
+        }
         st_bf16xCW<CW>(dst + i0, y0);
         st_bf16xCW<CW>(dst + DH / 2 + i0, y1);
       }
@@ -423,7 +434,7 @@ template <int BN, int DH, int EPI, bool PAIR>
 __device__ __forceinline__ void epilogue_heads_loop(uint32_t tmem_base, int q, int M, int N, const Sched& sc,
                                                     uint64_t* tfull, uint64_t* tempty, uint32_t leader_tempty,
                                                     const EpiArgs& ep) {
-  constexpr bool DEV = (EPI == EPI_DEV);
+  constexpr int MODE = EPI == EPI_DEV ? 1 : EPI == EPI_QKV_DEV ? 2 : 0;
   int it = 0;
   for (int u = sc.u0; u < sc.units; u += sc.ustep, ++it) {
     int mb, nb; tile_coords(u / sc.splits, sc.num_m, sc.num_n, sc.group_m, mb, nb);
@@ -436,9 +447,11 @@ __device__ __forceinline__ void epilogue_heads_loop(uint32_t tmem_base, int q, i
     tc_fence_after();
     const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN;
     unsigned long long dacc = 0;
-    epi_heads<BN, DH, DEV>(taddr, nb * BN, N, row_ok, row, ep, rr, dacc);
-    if constexpr (DEV) {
-      if (row_ok && ep.row_reuse[row]) atomicAdd(ep.dev_out + row, dacc);  // integer: order-independent
+    const int drow = (MODE == 2 && row_ok) ? ep.dev_row[row] : row;
+    const bool score = MODE != 0 && row_ok && ep.row_reuse[drow];
+    epi_heads<BN, DH, MODE>(taddr, nb * BN, N, row_ok, row, ep, rr, dacc, score);
+    if constexpr (MODE != 0) {
+      if (score) atomicAdd(ep.dev_out + drow, dacc);  // integer: order-independent
     }
     tc_fence_before();
     release_acc<PAIR>(tempty, acc, leader_tempty);
@@ -452,7 +465,7 @@ __device__ __forceinline__ void epilogue_loop(uint32_t tmem_base, int warp, int 
                                               const EpiArgs& ep, const CUtensorMap* tmC, uint8_t* sOut, int rank,
                                               int* s_flag) {
   const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-  if constexpr (EPI == EPI_QKV || EPI == EPI_DEV) {
+  if constexpr (EPI == EPI_QKV || EPI == EPI_DEV || EPI == EPI_QKV_DEV) {
     if (ep.head_dim == 128)
       epilogue_heads_loop<BN, 128, EPI, PAIR>(tmem_base, q, M, N, sc, tfull, tempty, leader_tempty, ep);
     else if (ep.head_dim == 64)
@@ -1173,6 +1186,7 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
       case EPI_SWIGLU: return launch_pair<EPI_SWIGLU>(a, b, c, M, N, K, ep, num_sms, s);
       case EPI_QKV: return launch_pair<EPI_QKV>(a, b, c, M, N, K, ep, num_sms, s);
       case EPI_DEV: return launch_pair<EPI_DEV>(a, b, c, M, N, K, ep, num_sms, s);
+      case EPI_QKV_DEV: return launch_pair<EPI_QKV_DEV>(a, b, c, M, N, K, ep, num_sms, s);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -1182,6 +1196,7 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   RC_GEMM_CASE(256, EPI_SWIGLU) RC_GEMM_CASE(256, EPI_QKV) RC_GEMM_CASE(256, EPI_DEV)
   RC_GEMM_CASE(128, EPI_BF16) RC_GEMM_CASE(128, EPI_F32) RC_GEMM_CASE(128, EPI_ADD_F32)
   RC_GEMM_CASE(128, EPI_QKV) RC_GEMM_CASE(128, EPI_DEV)
+  RC_GEMM_CASE(256, EPI_QKV_DEV) RC_GEMM_CASE(128, EPI_QKV_DEV)
 #undef RC_GEMM_CASE
   return cudaErrorInvalidValue;
 }

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
     int c = a.ucls[u_off + i];
     const bool in_win = window > 0 && pos >= n - window;
     if (in_win) c = CLS_FORCED;
+    if (a.u2s && a.u2s[u_off + i] < 0) c = CLS_PREFIX;  // gradual step: outside the previous Sel
     cls[i] = static_cast<uint8_t>(c);
     flag[i] = (c == CLS_FORCED) ? 1 : 0;
     mh += c == CLS_HIST;
@@ -225,6 +226,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(const SelectArgs a) {
     a.sel_pos[w] = P + i;
     a.sel_dst[w] = rq2.z + P + i;
     a.sel_urow[w] = u_off + i;
+    if (a.map) a.map[w] = a.u2s[u_off + i];
     ++w;
   }
 }
@@ -359,6 +361,12 @@ __global__ void k_resolve_hist(int4* __restrict__ meta, int32_t n, const uint64_
     }
     meta[i] = m;
   }
+}
+
+__global__ void k_scatter_index(int32_t* __restrict__ dst, const int32_t* __restrict__ idx, int32_t n) {
+  griddep_wait();
+  griddep_launch();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dst[idx[i]] = i;
 }
 
 __global__ void k_scatter_i32(int32_t* __restrict__ dst, const int2* __restrict__ idx_val, int32_t n) {
@@ -514,6 +522,11 @@ cudaError_t scatter_i32_launch(int32_t* dst, const int2* idx_val, int32_t n, cud
   if (n <= 0) return cudaSuccess;
   return launch_pdl(k_scatter_i32, dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024))), dim3(256), 0,
                     s, dst, idx_val, n);
+}
+cudaError_t scatter_index_launch(int32_t* dst, const int32_t* idx, int32_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(k_scatter_index, dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 1024))), dim3(256), 0,
+                    s, dst, idx, n);
 }
 cudaError_t vmap_identity_launch(int32_t* vmap, const int32_t* rows, int32_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;

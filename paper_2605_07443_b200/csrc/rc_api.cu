@@ -247,6 +247,9 @@ struct rc_ctx {
   int32_t* sel_pos = nullptr;
   int32_t* sel_dst = nullptr;
   int32_t* sel_urow = nullptr;
+  // gradual filtering (R-GF): second Sel arrays, U row -> previous Sel row, new -> previous Sel row
+  // (5 x Mx int32, allocated on first use)
+  int32_t* grad_buf = nullptr;
   // tensor maps
   CUtensorMap mA_a{}, mA_o{}, mA_h{};
   CUtensorMap mA_a64{}, mA_o64{}, mA_h64{};  // same operands, gemm_t_box_rows()-row boxes (transposed small-M GEMM)
@@ -290,7 +293,7 @@ struct rc_ctx {
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
                     a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
-                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt, vmap, proto_tab, dev_err};
+                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt, vmap, proto_tab, dev_err, grad_buf};
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
@@ -982,7 +985,9 @@ void rc_release(rc_ctx* c, int32_t n, const rc_seq* seqs) {
 namespace {
 struct ReqPlan {
   const Seq* sq;
-  int32_t u_off, u_cnt, sel_off, sel_cnt, k_h, k_i, forced, window;
+  int32_t u_off, u_cnt, sel_off, sel_cnt, k_h, k_i, forced, window;  // the final Sel
+  // gradual steps i = 0..g (R-GF); with g = 0 step 0 is the final Sel
+  int32_t g_cnt[RC_MAX_GRADUAL + 1], g_off[RC_MAX_GRADUAL + 1], g_kh[RC_MAX_GRADUAL + 1], g_ki[RC_MAX_GRADUAL + 1];
 };
 
 int32_t budget(int32_t r_bp, int32_t count) { return static_cast<int32_t>((static_cast<int64_t>(r_bp) * count + 9999) / 10000); }
@@ -997,8 +1002,21 @@ rc_status plan_requests(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_p
     return fail(RC_E_INVALID, "recompute ratio out of [0, 10000] bp");
   if (prm->check_layer < 0 || prm->check_layer >= c->m.n_layers) return fail(RC_E_INVALID, "check_layer out of range");
   if (prm->window < 0) return fail(RC_E_INVALID, "negative window");
+  const int G = prm->gradual_layers;
+  if (G < 0 || G > RC_MAX_GRADUAL) return fail(RC_E_INVALID, "gradual_layers out of [0, RC_MAX_GRADUAL]");
+  if (G > 0) {
+    if (prm->check_layer + G > c->m.n_layers - 1) return fail(RC_E_INVALID, "check_layer + gradual_layers beyond the last layer");
+    if (prm->r_start_rev_bp < prm->r_rev_bp || prm->r_start_rev_bp > 10000 || prm->r_start_item_bp < prm->r_item_bp ||
+        prm->r_start_item_bp > 10000)
+      return fail(RC_E_INVALID, "gradual start ratios must lie in [r, 10000] bp");
+  }
+  // R-GF: r_i = r_start - floor((r_start - r) i / g)
+  auto ratio = [&](int32_t r0, int32_t r, int i) {
+    return G == 0 ? r : r0 - static_cast<int32_t>((static_cast<int64_t>(r0) - r) * i / G);
+  };
   plan.resize(n_req);
   int32_t uo = 0, so = 0;
+  int32_t go[RC_MAX_GRADUAL + 1] = {};
   for (int r = 0; r < n_req; ++r) {
     auto it = c->seqs.find(seqs[r]);
     if (it == c->seqs.end()) return fail(RC_E_NOTFOUND, "unknown sequence handle");
@@ -1027,6 +1045,13 @@ rc_status plan_requests(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_p
     p.sel_cnt = p.forced + p.k_h + p.k_i;
     if (p.sel_cnt == 0 || sq.n - 1 < sq.P) return fail(RC_E_INVALID, "request has no recomputed position");
     p.sel_off = so;
+    for (int i = 0; i <= G; ++i) {
+      p.g_kh[i] = budget(ratio(prm->r_start_rev_bp, prm->r_rev_bp, i), nh);
+      p.g_ki[i] = budget(ratio(prm->r_start_item_bp, prm->r_item_bp, i), ni);
+      p.g_cnt[i] = p.forced + p.g_kh[i] + p.g_ki[i];
+      p.g_off[i] = go[i];
+      go[i] += p.g_cnt[i];
+    }
     uo += p.u_cnt;
     so += p.sel_cnt;
   }
@@ -1045,12 +1070,13 @@ rc_status rc_sel_count(rc_ctx* c, int32_t n_req, const rc_seq* seqs, const rc_pr
 }
 
 namespace {
-// one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
-rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
-                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min,
-                    bool paired, double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
+// first half of a decoder layer over `rows` rows: RMSNorm + QKV projection with fused RoPE,
+// q -> c->q, k/v -> arena rows d_dst. `dev` (gradual steps, R-GF): also score the k/v of the rows
+// with dev->row_reuse[dev->dev_row[row]] against the stitched arena values they overwrite.
+rc_status run_qkv(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_pos, const int32_t* d_dst,
+                  const EpiArgs* dev, cudaStream_t s) {
   const rc_model_desc& m = c->m;
-  const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
+  const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads;
   const double R = rows, norm_b = R * d * 6.0;
   RC_LAUNCH(RC_K_SMALL, 0, norm_b, -1, rmsnorm_launch(x, nullptr, rows, d, c->ln1[l], m.rms_eps, c->a, s));
   EpiArgs ep = epi_base(c);
@@ -1061,9 +1087,21 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
   ep.head_stride = c->pd.arena_rows * dh;
   ep.rope_cos = c->rope_cos; ep.rope_sin = c->rope_sin; ep.rope_zero = c->rope_zero;
   ep.n_heads = H; ep.n_kv_heads = Hk; ep.head_dim = dh;
+  if (dev) { ep.dev_out = dev->dev_out; ep.dev_row = dev->dev_row; ep.row_reuse = dev->row_reuse; }
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, c->Nqkv, d), gemm_bytes(R, c->Nqkv, d, 2), -1,
-            gemm_launch(&c->mA_a, &c->mB_qkv[l], nullptr, rows, c->Nqkv, d, c->bn_qkv, EPI_QKV, ep, c->num_sms, s,
-                        &c->mA_a64));
+            gemm_launch(&c->mA_a, &c->mB_qkv[l], nullptr, rows, c->Nqkv, d, c->bn_qkv, dev ? EPI_QKV_DEV : EPI_QKV, ep,
+                        c->num_sms, s, &c->mA_a64));
+  return RC_OK;
+}
+
+// second half: attention of the `rows` query rows (q in c->q, positions d_pos) over the arena,
+// O-projection + residual, RMSNorm, SwiGLU MLP + residual
+rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
+                   const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min, bool paired,
+                   double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
+  const rc_model_desc& m = c->m;
+  const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
+  const double R = rows, norm_b = R * d * 6.0;
   AttnArgs at{};
   at.q = c->q; at.o = c->o; at.qpos = d_pos; at.tiles = d_tiles; at.n_tiles = n_tiles;
   at.k = arena_layer(c, l, 0); at.v = arena_layer(c, l, 1); at.head_stride = c->pd.arena_rows * dh;
@@ -1124,6 +1162,16 @@ rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t r
             gemm_launch(&c->mA_h, &c->mB_d[l], mx, rows, d, F, c->bn_d, EPI_ADD_F32, ed, c->num_sms, s,
                         &c->mA_h64));
   return RC_OK;
+}
+
+// one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
+rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
+                    const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min,
+                    bool paired, double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
+  rc_status st = run_qkv(c, l, x, rows, d_pos, d_dst, nullptr, s);
+  if (st != RC_OK) return st;
+  return run_rest(c, l, x, mx, rows, d_pos, d_tiles, n_tiles, n_splits, split_min, paired, attn_flops, attn_pending,
+                  det, zc_layer, s);
 }
 }  // namespace
 
@@ -1200,6 +1248,16 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   // forced selection (test mode): validate
   const bool forced = prm->forced_sel != nullptr;
   const bool mass = !forced && prm->lambda < 1.0f;  // NEXT-1: Eq. 3 with the attention-mass term
+  const int G = prm->gradual_layers;                // R-GF gradual filtering steps
+  if (G > 0 && forced) return fail(RC_E_UNSUPPORTED, "gradual filtering with forced_sel");
+  if (G > 0 && c->zc_v) return fail(RC_E_UNSUPPORTED, "gradual filtering with zero-copy V (RC_ZERO_COPY_V)");
+  int32_t S_step[RC_MAX_GRADUAL + 1], trace_off[RC_MAX_GRADUAL + 2];
+  trace_off[0] = 0;
+  for (int i = 0; i <= G; ++i) {
+    S_step[i] = plan.back().g_off[i] + plan.back().g_cnt[i];
+    trace_off[i + 1] = trace_off[i] + S_step[i];
+  }
+  const int32_t S0 = S_step[0];
   if (forced) {
     if (!prm->forced_sel_off) return fail(RC_E_INVALID, "forced_sel needs forced_sel_off");
     for (int r = 0; r < n_req; ++r) {
@@ -1260,6 +1318,15 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   }
   n_ut *= split_u;
   n_st *= split_s;
+  // gradual steps 0..g-1: their own tile lists over Sel_i (launch shape of the final list)
+  int32_t n_gt[RC_MAX_GRADUAL + 1] = {};
+  size_t o_gt[RC_MAX_GRADUAL + 1] = {};
+  for (int i = 0; i < G; ++i) {
+    for (auto& p : plan) n_gt[i] += pair_s ? (ntiles(p.g_cnt[i]) + 1) / 2 * 2 : ntiles(p.g_cnt[i]);
+    n_gt[i] *= split_s;
+    o_gt[i] = lay.add(static_cast<size_t>(n_gt[i]) * 16);
+  }
+  const size_t o_rqg = lay.add(static_cast<size_t>(G) * n_req * 32);  // per step i >= 1: req, req2
   const size_t o_ut = lay.add(static_cast<size_t>(n_ut) * 16), o_st = lay.add(static_cast<size_t>(n_st) * 16),
                o_last = lay.add(n_req * 4), o_creq = lay.add(n_cand * 4), o_cid = lay.add(n_cand * 4),
                o_fsel = lay.add(forced ? static_cast<size_t>(S) * 12 : 0);
@@ -1279,6 +1346,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   int4* hut = reinterpret_cast<int4*>(hb + o_ut);
   int4* hst = reinterpret_cast<int4*>(hb + o_st);
   int iu = 0, is = 0, ic = 0, ikt = 0;
+  int kg[RC_MAX_GRADUAL + 1] = {};
   for (int r = 0; r < n_req; ++r) {
     const ReqPlan& p = plan[r];
     const Seq& sq = *p.sq;
@@ -1291,9 +1359,21 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
       hb[o_cls + p.u_off + i] = sq.cls[pos];
       hb[o_reuse + p.u_off + i] = (!in_win && (sq.cls[pos] == RC_TOK_HIST || sq.cls[pos] == RC_TOK_ITEM)) ? 1 : 0;
     }
-    hreq[r] = make_int4(p.u_off, p.u_cnt, p.sel_off, sq.n);
-    hreq2[r] = make_int4(p.k_h, p.k_i, static_cast<int>(sq.arena_row), p.window);
+    hreq[r] = make_int4(p.u_off, p.u_cnt, p.g_off[0], sq.n);  // step 0 (= the final Sel without gradual steps)
+    hreq2[r] = make_int4(p.g_kh[0], p.g_ki[0], static_cast<int>(sq.arena_row), p.window);
     const int arow = static_cast<int>(sq.arena_row);
+    for (int i = 1; i <= G; ++i) {
+      int4* rg = reinterpret_cast<int4*>(hb + o_rqg) + static_cast<size_t>(i - 1) * 2 * n_req;
+      rg[r] = make_int4(p.u_off, p.u_cnt, p.g_off[i], sq.n);
+      rg[n_req + r] = make_int4(p.g_kh[i], p.g_ki[i], arow, p.window);
+    }
+    for (int i = 0; i < G; ++i) {
+      int4* ht = reinterpret_cast<int4*>(hb + o_gt[i]);
+      int& k = kg[i];
+      for (int j = 0; j < p.g_cnt[i]; j += TQ)
+        for (int sp = 0; sp < split_s; ++sp) ht[k++] = make_int4(p.g_off[i] + j, std::min(TQ, p.g_cnt[i] - j), arow, sp);
+      if (pair_s && ntiles(p.g_cnt[i]) % 2) ht[k++] = make_int4(p.g_off[i] + p.g_cnt[i], 0, arow, 0);
+    }
     for (int i = 0; i < p.u_cnt; i += TQ)
       for (int sp = 0; sp < split_u; ++sp) hut[iu++] = make_int4(p.u_off + i, std::min(TQ, p.u_cnt - i), arow, sp);
     if (pair_u && ntiles(p.u_cnt) % 2) hut[iu++] = make_int4(p.u_off + p.u_cnt, 0, arow, 0);
@@ -1374,12 +1454,60 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   }
   if (c->zc_v)  // Sel rows get fresh K/V in the arena at the layers >= c
     RC_LAUNCH(RC_K_SMALL, 0, S * 8.0, -1, vmap_identity_launch(c->vmap, c->sel_dst, S, s));
-  RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(S) * d * 8.0, -1,
-            gather_rows_f32_launch(c->x, c->sel_urow, S, d, c->xs, s));
-  // ---- a5-a7: selective layers c..L-1 on Sel
+  if (prm->sel_trace)
+    RC_CUDA(cudaMemcpyAsync(prm->sel_trace, c->sel_pos, static_cast<size_t>(S0) * 4, cudaMemcpyDeviceToDevice, s));
+  RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(S0) * d * 8.0, -1,
+            gather_rows_f32_launch(c->x, c->sel_urow, S0, d, c->xs, s));
+  // ---- a5-a7: selective layers c..L-1 on Sel (gradual steps: layers c+1..c+g shrink it, R-GF)
+  int32_t *sp = c->sel_pos, *sd = c->sel_dst, *su = c->sel_urow;
+  int32_t *sp2 = nullptr, *sd2 = nullptr, *su2 = nullptr, *u2s = nullptr, *gmap = nullptr;
+  if (G > 0) {
+    if (!c->grad_buf) {
+      c->grad_buf = dev_alloc<int32_t>(static_cast<size_t>(c->Mx) * 5, &e);
+      if (e != cudaSuccess) { c->grad_buf = nullptr; return fail(RC_E_NOMEM, "gradual-filtering workspace"); }
+    }
+    sp2 = c->grad_buf; sd2 = sp2 + c->Mx; su2 = sd2 + c->Mx; u2s = su2 + c->Mx; gmap = u2s + c->Mx;
+  }
+  const int Hq = m.n_heads * m.head_dim;  // q row width (bf16), moved as Hq / 2 four-byte words
+  int32_t cur = S0;
   for (int l = cL; l < L; ++l) {
-    st = run_layer(c, l, c->xs, &c->mC_xs, S, c->sel_pos, c->sel_dst, d_st, n_st, split_s, smin_s, pair_s, 0.0, pend_idx,
-                   prm->deterministic ? 1 : 0, c->zc_v, s);
+    const int i = l - cL;
+    const int det = prm->deterministic ? 1 : 0;
+    const bool last_list = i >= G;  // the final Sel's tile list
+    const int4* tl = last_list ? d_st : reinterpret_cast<const int4*>(db + o_gt[i]);
+    const int32_t ntl = last_list ? n_st : n_gt[i];
+    if (i == 0 || i > G) {
+      st = run_layer(c, l, c->xs, &c->mC_xs, cur, sp, sd, tl, ntl, split_s, smin_s, pair_s, 0.0, pend_idx, det, c->zc_v, s);
+      if (st != RC_OK) return st;
+      continue;
+    }
+    // gradual step i: q/k/v of Sel_{i-1}, scored against the stitched k/v they overwrite
+    RC_CUDA(cudaMemsetAsync(c->dev, 0, static_cast<size_t>(U) * 8, s));
+    RC_CUDA(cudaMemsetAsync(u2s, 0xFF, static_cast<size_t>(U) * 4, s));
+    RC_LAUNCH(RC_K_SMALL, 0, cur * 8.0, -1, scatter_index_launch(u2s, su, cur, s));
+    EpiArgs dv{};
+    dv.dev_out = c->dev; dv.dev_row = su; dv.row_reuse = reinterpret_cast<const uint8_t*>(db + o_reuse);
+    st = run_qkv(c, l, c->xs, cur, sp, sd, &dv, s);
+    if (st != RC_OK) return st;
+    const int4* rg = reinterpret_cast<const int4*>(db + o_rqg) + static_cast<size_t>(i - 1) * 2 * n_req;
+    SelectArgs sa{};
+    sa.dev = c->dev; sa.ucls = reinterpret_cast<const uint8_t*>(db + o_cls);
+    sa.req = rg; sa.req2 = rg + n_req;
+    sa.n_req = n_req; sa.sel_pos = sp2; sa.sel_dst = sd2; sa.sel_urow = su2;
+    sa.u2s = u2s; sa.map = gmap;
+    RC_LAUNCH(RC_K_SELECT, 0, static_cast<double>(U) * 13.0, -1, select_launch(sa, s));
+    const int32_t nxt = S_step[i];
+    // compact the residual rows and the query rows of Sel_i (through scratch: x of U, o)
+    RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(nxt) * d * 8.0, -1, gather_rows_f32_launch(c->xs, gmap, nxt, d, c->x, s));
+    RC_CUDA(cudaMemcpyAsync(c->xs, c->x, static_cast<size_t>(nxt) * d * 4, cudaMemcpyDeviceToDevice, s));
+    RC_LAUNCH(RC_K_SMALL, 0, static_cast<double>(nxt) * Hq * 4.0, -1,
+              gather_rows_f32_launch(reinterpret_cast<const float*>(c->q), gmap, nxt, Hq / 2, reinterpret_cast<float*>(c->o), s));
+    RC_CUDA(cudaMemcpyAsync(c->q, c->o, static_cast<size_t>(nxt) * Hq * 2, cudaMemcpyDeviceToDevice, s));
+    std::swap(sp, sp2); std::swap(sd, sd2); std::swap(su, su2);
+    cur = nxt;
+    if (prm->sel_trace)
+      RC_CUDA(cudaMemcpyAsync(prm->sel_trace + trace_off[i], sp, static_cast<size_t>(nxt) * 4, cudaMemcpyDeviceToDevice, s));
+    st = run_rest(c, l, c->xs, &c->mC_xs, cur, sp, tl, ntl, split_s, smin_s, pair_s, 0.0, pend_idx, det, false, s);
     if (st != RC_OK) return st;
   }
   // ---- a8: final norm on each request's last position, LM head, candidate readout
@@ -1407,10 +1535,10 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
     pd.S = S;
     pd.layers = L - cL;
     if (cudaMallocHost(&pd.host, static_cast<size_t>(S) * 4) != cudaSuccess) return fail(RC_E_NOMEM, "profile buffer");
-    RC_CUDA(cudaMemcpyAsync(pd.host, c->sel_pos, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
+    RC_CUDA(cudaMemcpyAsync(pd.host, sp, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToHost, s));
     c->pend.push_back(std::move(pd));
   }
-  if (sel_pos_out) RC_CUDA(cudaMemcpyAsync(sel_pos_out, c->sel_pos, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToDevice, s));
+  if (sel_pos_out) RC_CUDA(cudaMemcpyAsync(sel_pos_out, sp, static_cast<size_t>(S) * 4, cudaMemcpyDeviceToDevice, s));
   if (hidden) RC_CUDA(cudaMemcpyAsync(hidden, c->xs, static_cast<size_t>(S) * d * 4, cudaMemcpyDeviceToDevice, s));
   // every kernel of the layer loop reads the slot's device tables (tiles, positions, rows):
   // the slot is reusable once the last of them has run (the event is waited on by the host)

@@ -65,6 +65,8 @@ enum EpiKind : int {
   EPI_SWIGLU = 3,   // B rows [g0 u0 g1 u1 ...] -> out bf16 [M][ldo] = silu(g) * u
   EPI_QKV = 4,      // packed [q | k | v] heads (dims [0, dh/2, 1, dh/2+1, ..]): RoPE at pos[row] on q,k; q -> q_out, k,v -> arena
   EPI_DEV = 5,      // packed [k | v] heads: RoPE on k, bf16 round, fixed-point |new - stitched| -> dev[row]
+  EPI_QKV_DEV = 6,  // EPI_QKV that first scores k, v against the stitched arena rows it overwrites:
+                    // |new - stitched| -> dev[dev_row[row]] where row_reuse[dev_row[row]] (gradual steps)
 };
 
 struct EpiArgs {
@@ -83,7 +85,8 @@ struct EpiArgs {
   int32_t rope_zero = 0;
   int32_t n_heads = 0, n_kv_heads = 0, head_dim = 0;
   unsigned long long* dev_out = nullptr;  // [M]
-  const uint8_t* row_reuse = nullptr;     // [M]
+  const uint8_t* row_reuse = nullptr;     // [M] (EPI_QKV_DEV: indexed through dev_row)
+  const int32_t* dev_row = nullptr;       // EPI_QKV_DEV: [M] GEMM row -> index into dev_out / row_reuse
   VSrc vsrc;                              // DEV: where the stitched V rows live (zero-copy V)
   // residual epilogues: workspace for partial tiles (split-K / stream-K) summed in K order by the
   // last-arriving CTA of a tile (bitwise-reproducible x); counters zero between launches
@@ -245,7 +248,13 @@ struct SelectArgs {
   const int4* req2;               // per request {k_hist, k_item, arena_base, window}
   int32_t n_req;
   int32_t* sel_pos; int32_t* sel_dst; int32_t* sel_urow;
+  // gradual steps (reading R-GF): u2s[U row] = the row's index in the previous Sel, -1 outside it
+  // (those rows are no candidates); map[new Sel row] = its index in the previous Sel. NULL = one shot
+  const int32_t* u2s = nullptr;
+  int32_t* map = nullptr;
 };
+// dst[idx[j]] = j for j < n
+cudaError_t scatter_index_launch(int32_t* dst, const int32_t* idx, int32_t n, cudaStream_t s);
 cudaError_t dev_diag_launch(const uint16_t* kn, const uint16_t* ks, const uint16_t* vn, const uint16_t* vs, int32_t n,
                             int32_t width, unsigned long long* out, cudaStream_t s);
 cudaError_t select_launch(const SelectArgs& a, cudaStream_t s);
