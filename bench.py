@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--check-layer", type=int, default=1)
     ap.add_argument("--lam", type=float, default=1.0,
                     help="Eq. 3 lambda: 1 = deviation only (default, R3); < 1 adds the attention-mass term (NEXT-1)")
+    ap.add_argument("--gradual", type=int, default=0,
+                    help="gradual filtering steps g (reading R-GF, NEXT-1 variant): Sel shrinks from --r-start at "
+                         "the check layer to r at layer c + g; 0 = one-shot selection (default)")
+    ap.add_argument("--r-start", type=int, default=0, help="gradual: ratio (bp) at the check layer")
     ap.add_argument("--distinct-batches", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--flashinfer", action="store_true",
@@ -108,6 +112,14 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload setup
+def gradual_kw(args, r_bp):
+    """selective_prefill keyword arguments of the gradual-filtering variant (R-GF), {} when off."""
+    if not args.gradual:
+        return {}
+    r0 = max(args.r_start, r_bp)
+    return {"gradual": args.gradual, "r_start_rev_bp": r0, "r_start_item_bp": r0}
+
+
 def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
     """§8(e): Alg. 1 placement of the catalog over `world` GPUs (historical trace: 2000 seeded
     requests), Eq. 2 routing of one global request stream; this rank keeps the requests routed
@@ -486,7 +498,7 @@ def run_ours(args, wl):
             side.wait_stream(stream)
             fetch_host(i + 1)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
-                              out=out, stream=stream, lam=args.lam)
+                              out=out, stream=stream, lam=args.lam, **gradual_kw(args, r_bp))
         ctx.release(seqs)
 
     for i in range(args.warmup):
@@ -596,6 +608,8 @@ def run_ours(args, wl):
                       "seq_len": ("mixed " + "/".join(f"{w.n}:{f:.0%}" for w, f in args.mix)) if args.mix else wl.n,
                       "r": r_bp / 1e4, "check_layer": c,
                       "lambda": args.lam,
+                      **({"gradual": {"layers": args.gradual, "r_start": max(args.r_start, r_bp) / 1e4}}
+                         if args.gradual else {}),
                       "parallelism": (f"dp{world}: Alg. 1 sharded item pool, Eq. 2 routing, NVLink fetch"
                                       if world > 1 else "dp1"),
                       "l2": "inputs larger than L2 (16 GB weights + item pool per GPU)",
@@ -671,7 +685,7 @@ def baselines(args, wl, env, r_bp, c, step_ms):
         seqs = ctx.assemble(lays, prefix_id=1, gather_from=c)
         n_cand = sum(len(l["cand_idtok"]) for l in lays)
         ctx.selective_prefill(seqs, rbp, rbp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
-                              lam=args.lam if rbp < 10000 else 1.0)
+                              lam=args.lam if rbp < 10000 else 1.0, **(gradual_kw(args, rbp) if rbp < 10000 else {}))
         ctx.release(seqs)
 
     B = len(batches[0])
@@ -775,7 +789,8 @@ def run_poisson(args, wl):
             fetched.append(len(f))
         seqs = ctx.assemble(batch_lays, prefix_id=1, gather_from=c, stream=stream)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False,
-                              n_cand=sum(len(l["cand_idtok"]) for l in batch_lays), stream=stream)
+                              n_cand=sum(len(l["cand_idtok"]) for l in batch_lays), stream=stream,
+                              **gradual_kw(args, r_bp))
         ctx.release(seqs)
 
     for k in range(3 if n > 0 else 0):  # warm-up at the largest batch
@@ -848,6 +863,8 @@ def main():
     else:
         args.mix = None
         wl = rcgen.WORKLOADS[args.config]
+    if args.gradual:  # the CPU sample times the one-shot oracle: not this variant's baseline
+        args.no_cpu_baseline = True
     if args.impl == "reference":
         run_reference(args, wl)
     elif args.poisson_qps > 0:
