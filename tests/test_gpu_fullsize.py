@@ -37,7 +37,7 @@ _LOGITS = {}
 CHECK_REQS = tuple(int(x) for x in os.environ.get("RC_FULLSIZE_REQS", "0,31").split(","))
 
 
-def _setup(wl, batch, check_reqs, materialize=False):
+def _setup(wl, batch, check_reqs, materialize=False, gkw=None):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2605_07443_b200.build import build
@@ -78,7 +78,8 @@ def _setup(wl, batch, check_reqs, materialize=False):
                                  [cat.tokens[int(i)] for i in r.cand_items], r.tail_tokens) for r in reqs]
     seqs = ctx.assemble(lays, prefix_id=1, gather_from=C)
     n_cand = sum(len(l["cand_idtok"]) for l in lays)
-    out = ctx.selective_prefill(seqs, R_BP, R_BP, check_layer=C, hidden=True, n_cand=n_cand)
+    out = ctx.selective_prefill(seqs, R_BP, R_BP, check_layer=C, hidden=True, n_cand=n_cand,
+                                **(dict(gkw, sel_trace=True) if gkw else {}))
     torch.cuda.synchronize()
     res = {k: (v.cpu().numpy() if torch.is_tensor(v) else v) for k, v in out.items()}
     res["kv_last"] = {r: tuple(t.cpu().numpy().view(np.uint16) for t in ctx.read_kv(seqs[r], shape.n_layers - 1, n))
@@ -87,7 +88,7 @@ def _setup(wl, batch, check_reqs, materialize=False):
     ctx.release(seqs)
     # run-to-run determinism: the same batch assembled and prefilled again, in the default mode and
     # twice with every residual sum order-fixed (deterministic=1)
-    for key, det in (("rerun", False), ("det1", True), ("det2", True)):
+    for key, det in (() if gkw else (("rerun", False), ("det1", True), ("det2", True))):
         seqs = ctx.assemble(lays, prefix_id=1, gather_from=C)
         out2 = ctx.selective_prefill(seqs, R_BP, R_BP, check_layer=C, hidden=True, n_cand=n_cand, deterministic=det)
         torch.cuda.synchronize()
@@ -252,4 +253,50 @@ def test_cfg3_batch1_materialized_pools_matches_oracle():
            "K_last": rel_l2(Kg, forced["K"][d["shape"].n_layers - 1][sel])}
     print("fullsize cfg3 batch-1 materialised-pool parity", json.dumps(err))
     assert jac >= 0.95, err
+    assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
+
+
+def test_cfg3_batch1_gradual_filtering_matches_oracle():
+    """Gradual filtering (R-GF) in the launch configuration `bench.py --batch 1 --gradual 2 --r-start
+    3000` times: Sel at 30 % of each class at the check layer, 22.5 % at layer 2, 15 % from layer 3 on,
+    on model-materialised pools. The oracle runs along the GPU's own trajectory (sel_trace): every step
+    is nested with the step budgets, each step's members are the oracle's top-k of its own layer-l
+    divergence among the previous step (Jaccard >= 0.95: bf16 noise may flip near ties), step 0 matches
+    the oracle's one-shot choice at 30 %, and logits, x_L[Sel] and the last layer's K/V at Sel stay
+    within the north-star bounds."""
+    from oracle.select import select_sel, gradual_ratio_bp
+    g, r0 = 2, 3000
+    gkw = dict(gradual=g, r_start_rev_bp=r0, r_start_item_bp=r0)
+    res, d = _setup(rcgen.CFG3, 1, (0,), materialize=True, gkw=gkw)
+    L = d["shape"].n_layers
+    off, trace = res["trace_off"], res["sel_trace"]
+    steps = [trace[off[i]:off[i + 1]] for i in range(g + 1)]
+    sel = res["sel_pos"]
+    assert np.array_equal(steps[-1], sel)
+    req = d["reqs"][0]
+    lay = layout_from_request(req, d["cat"], d["sys"])
+    ids = [int(i) for i in req.cand_items]
+    item_d = {it: (d["item_kv"][it], d["wl"].prefix_len) for it in ids}
+    K, V, _ = assemble(d["shape"], lay, item_d, d["hist"], d["pkv"], gather_from=C)
+    forced = selective_prefill(OracleModel(d["shape"], d["W"]), lay, K, V, R_BP, R_BP, check_layer=C,
+                               forced_steps=steps, **gkw)
+    sub = dataclasses.replace(d["shape"], n_layers=C + 1)
+    own0 = selective_prefill(OracleModel(sub, dict(d["W"], layers=d["W"]["layers"][:C + 1])), lay, K[:C + 1],
+                             V[:C + 1], r0, r0, check_layer=C)["sel"]
+
+    def jac(a, b):
+        a, b = set(int(x) for x in a), set(int(x) for x in b)
+        return len(a & b) / len(a | b)
+    err = {"jaccard_step0": jac(steps[0], own0), "sizes": [len(x) for x in steps]}
+    for i in range(1, g + 1):
+        assert set(steps[i].tolist()) <= set(steps[i - 1].tolist())
+        r_i = gradual_ratio_bp(r0, R_BP, i, g)
+        ref = select_sel(lay.cls, forced["D_steps"][i], r_i, r_i, 0, among=steps[i - 1])
+        assert len(ref) == len(steps[i])
+        err[f"jaccard_step{i}"] = jac(steps[i], ref)
+    Kg = bf16_to_f32(res["kv_last"][0][0])[sel].astype(np.float64)
+    err.update(logits=rel_l2(res["logits"][0], forced["logits"]), hidden=rel_l2(res["hidden"], forced["x_sel"]),
+               K_last=rel_l2(Kg, forced["K"][L - 1][sel]))
+    print("fullsize cfg3 batch-1 gradual parity", json.dumps(err))
+    assert all(err[f"jaccard_step{i}"] >= 0.95 for i in range(g + 1)), err
     assert err["hidden"] < TOL and err["K_last"] < TOL and err["logits"] < LOGITS_TOL_PER_REQUEST, err
