@@ -45,6 +45,8 @@ def parse():
                     help="gradual filtering steps g (reading R-GF, NEXT-1 variant): Sel shrinks from --r-start at "
                          "the check layer to r at layer c + g; 0 = one-shot selection (default)")
     ap.add_argument("--r-start", type=int, default=0, help="gradual: ratio (bp) at the check layer")
+    ap.add_argument("--attn-kernel", type=int, default=0,
+                    help="rc_prefill_params.attn_kernel (RC_ATTN_*): 0 = AUTO (default); others for A/B runs")
     ap.add_argument("--distinct-batches", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--flashinfer", action="store_true",
@@ -498,7 +500,8 @@ def run_ours(args, wl):
             side.wait_stream(stream)
             fetch_host(i + 1)
         ctx.selective_prefill(seqs, r_bp, r_bp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
-                              out=out, stream=stream, lam=args.lam, **gradual_kw(args, r_bp))
+                              out=out, stream=stream, lam=args.lam, attn_kernel=args.attn_kernel,
+                              **gradual_kw(args, r_bp))
         ctx.release(seqs)
 
     for i in range(args.warmup):
@@ -685,7 +688,8 @@ def baselines(args, wl, env, r_bp, c, step_ms):
         seqs = ctx.assemble(lays, prefix_id=1, gather_from=c)
         n_cand = sum(len(l["cand_idtok"]) for l in lays)
         ctx.selective_prefill(seqs, rbp, rbp, check_layer=c, sel_pos=False, hidden=False, n_cand=n_cand,
-                              lam=args.lam if rbp < 10000 else 1.0, **(gradual_kw(args, rbp) if rbp < 10000 else {}))
+                              lam=args.lam if rbp < 10000 else 1.0, attn_kernel=args.attn_kernel if rbp < 10000 else 0,
+                              **(gradual_kw(args, rbp) if rbp < 10000 else {}))
         ctx.release(seqs)
 
     B = len(batches[0])

@@ -35,7 +35,8 @@ constexpr int NTHREADS = 128 + 256;        // 4 control warps + 2 x 4 softmax wa
 constexpr int KST = 2, VST = 2;
 constexpr uint32_t OFF_Q = 0, OFF_K = TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
 constexpr uint32_t OFF_RED = OFF_BAR + 256;  // [2 halves][2 (m, l)][128 rows] f32 for the final merge
-constexpr uint32_t SMEM_BYTES = OFF_RED + 2 * 2 * 128 * 4;
+constexpr uint32_t OFF_FLAG = OFF_RED + 2 * 2 * 128 * 4;  // KV split: "this CTA merges" flag
+constexpr uint32_t SMEM_BYTES = OFF_FLAG + 16;
 constexpr uint32_t O_COL = 256;            // O_h at 256 + 128 h
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 // every 2^x of P on the SFU: measured at cfg3 batch 1, 1.49 ms per step vs 1.62 with 3/8 on the FMA pipe
@@ -80,11 +81,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
   griddep_launch();
   // tiles of a request are in position order and the causal KV grows with position: launch them
-  // last-first, so the longest tiles start in the first wave and short ones fill the tail
-  const int tix = gridDim.x - 1 - blockIdx.x;
+  // last-first, every KV head of a tile next to each other, so the longest tiles of all heads start
+  // in the first wave and short ones fill the tail (longest-processing-time order over the machine)
+  const int tix = a.n_tiles - 1 - static_cast<int>(blockIdx.x) / a.n_kv_heads;
+  const int kvh = static_cast<int>(blockIdx.x) % a.n_kv_heads;
   const int4 tile = a.tiles[tix];
   const int row_start = tile.x, n_rows = tile.y, kv_base = tile.z;
-  const int kvh = blockIdx.y;
   const int G = a.n_heads / a.n_kv_heads;
   const int TQ = ROWS / G;
   const int H = a.n_heads;
@@ -268,10 +270,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tc_fence_after();
     const bool split = nsp > 1;
-    if (a.split_min > 0 && tile.w == 0 && r == 0 && h == 0)
-      a.split_flag[(tix / a.n_splits) * a.n_kv_heads + kvh] = split ? 1 : 0;
     // this thread writes output columns [h*64, h*64 + 64) of its row: bf16 into o, or (KV split) the
-    // fp32 partial normalised by its own l plus (m, l) for the merge kernel
+    // fp32 partial normalised by its own l plus (m, l); the split CTA of a tile that finishes last
+    // merges them (no merge kernel)
     uint16_t* dst = a.o + static_cast<int64_t>(row_start + t) * H * DH + (kvh * G + g) * DH + h * 64;
     const int64_t prow = (static_cast<int64_t>(tix) * a.n_kv_heads + kvh) * ROWS + r;
     float* pdst = split ? a.part_o + prow * DH + h * 64 : nullptr;
@@ -307,6 +308,53 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
+    if (split) {  // arrival count per (logical tile, KV head); the last split CTA merges and resets it
+      int* flag = reinterpret_cast<int*>(smem + OFF_FLAG);
+      __threadfence();
+      asm volatile("bar.sync 9, 256;" ::: "memory");
+      if (warp == 4 && lane == 0) {
+        int* ctr = a.split_flag + (tix / a.n_splits) * a.n_kv_heads + kvh;
+        const int last = atomicAdd(ctr, 1) == nsp - 1;
+        if (last) *ctr = 0;
+        *flag = last;
+      }
+      asm volatile("bar.sync 9, 256;" ::: "memory");
+      if (*flag && valid) {
+        __threadfence();
+        const int64_t prow0 = (static_cast<int64_t>(tix / a.n_splits * a.n_splits) * a.n_kv_heads + kvh) * ROWS + r;
+        const int64_t pstride = static_cast<int64_t>(a.n_kv_heads) * ROWS;  // next split of the same tile
+        float mm = -INFINITY;
+        for (int s2 = 0; s2 < nsp; ++s2) {
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (prow0 + s2 * pstride) * 2));
+          if (v.y > 0.f) mm = fmaxf(mm, v.x);
+        }
+        float wts[8], wsum = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) {
+          wts[s2] = 0.f;
+          if (s2 >= nsp) continue;
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (prow0 + s2 * pstride) * 2));
+          if (v.y > 0.f) wts[s2] = v.y * fast_exp2(v.x - mm);
+          wsum += wts[s2];
+        }
+        const float inv2 = wsum > 0.f ? 1.f / wsum : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 8) {
+          float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int s2 = 0; s2 < nsp; ++s2) {
+            if (wts[s2] == 0.f) continue;
+            const float4* src = reinterpret_cast<const float4*>(a.part_o + (prow0 + s2 * pstride) * DH + h * 64 + c);
+            const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+            acc[0] += wts[s2] * x0.x; acc[1] += wts[s2] * x0.y; acc[2] += wts[s2] * x0.z; acc[3] += wts[s2] * x0.w;
+            acc[4] += wts[s2] * x1.x; acc[5] += wts[s2] * x1.y; acc[6] += wts[s2] * x1.z; acc[7] += wts[s2] * x1.w;
+          }
+          uint4 u;
+          u.x = pack_bf2(acc[0] * inv2, acc[1] * inv2); u.y = pack_bf2(acc[2] * inv2, acc[3] * inv2);
+          u.z = pack_bf2(acc[4] * inv2, acc[5] * inv2); u.w = pack_bf2(acc[6] * inv2, acc[7] * inv2);
+          *reinterpret_cast<uint4*>(dst + c) = u;
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -314,52 +362,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
-// KV-split merge: out = sum_s w_s O_s / sum_s w_s, w_s = l_s 2^(m_s - max m). One thread per
-// (row, 8-column chunk) of a logical query tile; splits with l_s = 0 (no visible keys) are skipped.
-__global__ void __launch_bounds__(256) k_attn_merge(const AttnArgs a) {
-  griddep_wait();  // PDL: inputs of the previous kernel are complete and visible
-  griddep_launch();
-  const int t_log = blockIdx.x, kvh = blockIdx.y, S = a.n_splits;
-  if (a.split_min > 0 && a.split_flag[t_log * a.n_kv_heads + kvh] == 0) return;  // ran unsplit: O written
-  const int4 tile = a.tiles[t_log * S];
-  const int G = a.n_heads / a.n_kv_heads, TQ = ROWS / G;
-  // blockIdx.z picks a 16-row slab: 16 rows x 16 chunks = one unit per thread, so every split's
-  // partial is loaded in one round trip (the merge is latency-, not bandwidth-bound)
-  const int r = blockIdx.z * 16 + threadIdx.x / (DH / 8), c = (threadIdx.x % (DH / 8)) * 8;
-  const int t = r / G, g = r % G;
-  if (r >= TQ * G || t >= tile.y) return;
-  float ml[2 * 8];
-  float4 x[2 * 8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    if (s < S) {
-      const int64_t prow = (static_cast<int64_t>(t_log * S + s) * a.n_kv_heads + kvh) * ROWS + r;
-      const float2 v = *reinterpret_cast<const float2*>(a.part_ml + prow * 2);
-      ml[2 * s] = v.x; ml[2 * s + 1] = v.y;
-      x[2 * s] = reinterpret_cast<const float4*>(a.part_o + prow * DH + c)[0];
-      x[2 * s + 1] = reinterpret_cast<const float4*>(a.part_o + prow * DH + c)[1];
-    }
-  }
-  float m = -INFINITY;
-#pragma unroll
-  for (int s = 0; s < 8; ++s)
-    if (s < S && ml[2 * s + 1] > 0.f) m = fmaxf(m, ml[2 * s]);
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    if (s >= S || !(ml[2 * s + 1] > 0.f)) continue;
-    const float w = ml[2 * s + 1] * fast_exp2(ml[2 * s] - m);
-    const float4 x0 = x[2 * s], x1 = x[2 * s + 1];
-    acc[0] += w * x0.x; acc[1] += w * x0.y; acc[2] += w * x0.z; acc[3] += w * x0.w;
-    acc[4] += w * x1.x; acc[5] += w * x1.y; acc[6] += w * x1.z; acc[7] += w * x1.w;
-    wsum += w;
-  }
-  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-  uint4 u;
-  u.x = pack_bf2(acc[0] * inv, acc[1] * inv); u.y = pack_bf2(acc[2] * inv, acc[3] * inv);
-  u.z = pack_bf2(acc[4] * inv, acc[5] * inv); u.w = pack_bf2(acc[6] * inv, acc[7] * inv);
-  *reinterpret_cast<uint4*>(a.o + static_cast<int64_t>(tile.x + t) * a.n_heads * DH + (kvh * G + g) * DH + c) = u;
-}
 }  // namespace
 
 int attn_tc_tokens_per_tile(int group) { return ROWS / group; }
@@ -368,10 +370,9 @@ cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const
                            int64_t t_cap, cudaStream_t s) {
   if (a.n_tiles <= 0) return cudaSuccess;
   if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_attn_tc), SMEM_BYTES); e != cudaSuccess) return e;
-  dim3 grid(a.n_tiles, a.n_kv_heads);
-  cudaError_t e = launch_pdl(k_attn_tc, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV, a, t_cap);
-  if (e != cudaSuccess || a.n_splits <= 1) return e;
-  return launch_pdl(k_attn_merge, dim3(a.n_tiles / a.n_splits, a.n_kv_heads, ROWS / 16), dim3(256), 0, s, a);
+  if (a.n_splits > 8) return cudaErrorInvalidValue;
+  return launch_pdl(k_attn_tc, dim3(a.n_tiles * a.n_kv_heads), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV, a,
+                    t_cap);
 }
 
 int attn_tc_choose_splits(int n_tiles, int n_kv_heads, int est_kv_tiles, int num_sms, int* split_min) {

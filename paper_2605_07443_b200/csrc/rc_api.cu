@@ -241,7 +241,7 @@ struct rc_ctx {
   int64_t logits_rows = 0;
   float* part_o = nullptr;   // KV-split attention partials
   float* part_ml = nullptr;
-  int32_t* part_flag = nullptr;  // adaptive split: which logical tiles were split
+  int32_t* part_flag = nullptr;  // KV split: arrival counter per (logical tile, KV head)
   int32_t* attn_ctr = nullptr;   // paired attention work counter
   size_t part_rows = 0;
   int32_t* sel_pos = nullptr;
@@ -1122,13 +1122,13 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
       c->part_o = dev_alloc<float>(need * 128, &e);
       if (e == cudaSuccess) c->part_ml = dev_alloc<float>(need * 2, &e);
       if (e == cudaSuccess) c->part_flag = dev_alloc<int32_t>(static_cast<size_t>(n_tiles) * Hk, &e);
+      if (e == cudaSuccess) e = cudaMemset(c->part_flag, 0, static_cast<size_t>(n_tiles) * Hk * sizeof(int32_t));
       if (e != cudaSuccess) { c->part_rows = 0; return fail(RC_E_NOMEM, "attention split workspace"); }
       c->part_rows = need;
     }
     at.part_o = c->part_o;
     at.part_ml = c->part_ml;
-    at.split_flag = c->part_flag;
-    c->launches += 1;  // the merge kernel
+    at.split_flag = c->part_flag;  // per (logical tile, KV head) arrival counters, zero between launches
   }
   if (paired && !c->attn_ctr) {  // persistent paired kernel's work counter (reset by its last CTA)
     cudaError_t e = cudaSuccess;

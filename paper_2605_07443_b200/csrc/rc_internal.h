@@ -185,7 +185,7 @@ struct AttnArgs {
   float* part_ml = nullptr;  // [n_tiles][Hk][128][2]
   float* lse_out = nullptr;  // optional [R][H]: m + log2(l) per query row (k_attn_tc, n_splits = 1; NEXT-1)
   int32_t split_min = 0;     // > 0 with n_splits = 2: adaptive split (tiles under split_min KV tiles unsplit)
-  int32_t* split_flag = nullptr;  // [n_tiles / n_splits][Hk]: 1 = the tile was split (adaptive mode)
+  int32_t* split_flag = nullptr;  // [n_tiles / n_splits][Hk]: split CTAs' arrival counters (zero between launches)
   int32_t* work_ctr = nullptr;    // paired kernel: {next work item, finished CTAs}, zero between launches
   VSrc vsrc;                      // zero-copy V: V rows through vmap (cp.async loads) instead of TMA boxes
 };
