@@ -168,7 +168,11 @@ typedef struct rc_prefill_params {
                                  sizes: rc_sel_count at r_i); NULL = none */
 } rc_prefill_params;
 enum { RC_MAX_GRADUAL = 16 };
-enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3, RC_ATTN_ADAPTIVE = 4 };
+enum { RC_ATTN_AUTO = 0, RC_ATTN_SINGLE = 1, RC_ATTN_PAIRED = 2, RC_ATTN_SPLIT2 = 3, RC_ATTN_ADAPTIVE = 4,
+       RC_ATTN_CHUNKED = 5 };
+/* RC_ATTN_CHUNKED: the persistent paired kernel with every pair's causal KV range cut into chunks
+   sized on the device so that all (pair, KV head, chunk) items fill the SMs about twice; partials
+   merged by the last-arriving chunk (small grids, e.g. one request's selected rows at batch 1) */
 /* RC_ATTN_SPLIT2: every query tile's KV range in two CTAs + merge; RC_ATTN_ADAPTIVE: the same launch,
    but tiles shorter than half the longest prompt's KV run unsplit (decided on the device from the
    selected positions; measured slower than unsplit at cfg3 batch 1, so AUTO does not choose it) */

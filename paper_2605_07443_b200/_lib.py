@@ -52,7 +52,7 @@ class Prompt(C.Structure):
                 ("cand_tokens", I32P), ("n_tail", C.c_int32), ("tail_tokens", I32P)]
 
 
-RC_ATTN_AUTO, RC_ATTN_SINGLE, RC_ATTN_PAIRED, RC_ATTN_SPLIT2, RC_ATTN_ADAPTIVE = 0, 1, 2, 3, 4
+RC_ATTN_AUTO, RC_ATTN_SINGLE, RC_ATTN_PAIRED, RC_ATTN_SPLIT2, RC_ATTN_ADAPTIVE, RC_ATTN_CHUNKED = 0, 1, 2, 3, 4, 5
 
 
 class PrefillParams(C.Structure):

@@ -35,7 +35,12 @@ constexpr int NTHREADS = 128 + 256;       // 4 control warps + 2 x 4 softmax war
 constexpr int KST = 2, VST = 2;
 constexpr uint32_t OFF_Q = 0, OFF_K = 2 * TILE, OFF_V = OFF_K + KST * TILE, OFF_BAR = OFF_V + VST * TILE;
 constexpr uint32_t OFF_ITEM = OFF_BAR + 256;  // [2] work-item slots (scheduler -> roles)
-constexpr uint32_t SMEM_BYTES = OFF_ITEM + 16;
+// KV-chunked launches: per-CTA schedule table (pairs ranked by chunk length, first item of each rank,
+// KV tiles per pair, chunks per pair, chunk length) and the two tiles' "this CTA merges" flags
+constexpr int MAXP = ATTN_CHUNK_MAX_PAIRS;
+constexpr uint32_t OFF_SCHED = OFF_ITEM + 16;
+constexpr uint32_t SCHED_INTS = MAXP + (MAXP + 1) + MAXP + MAXP + 1 + 2;
+constexpr uint32_t SMEM_BYTES = OFF_SCHED + ((SCHED_INTS * 4 + 15) & ~15u);
 constexpr uint32_t O_COL = 256;            // O_t at 256 + 128 t
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 // 2 of 8 key chunks take 2^x on the FMA pipe: measured at cfg3 batch 32, 39.4 ms per step vs 40.3
@@ -104,20 +109,103 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int n_items = n_pairs * a.n_kv_heads;
   // item w: kv head w % Hk of pair n_pairs - 1 - w / Hk (a request's pairs are in position order, so
   // the longest causal pairs come first)
-  struct Item { int4 tl[2]; int nk[2]; int nkv, kv_base, kvh; };
+  // an item covers the KV tiles [c0, c0 + nkv) of its pair; nk[t] of them (from c0) are tile t's,
+  // whose causal range ends at its last row's position. nch[t] > 1: tile t's range is cut into nch[t]
+  // chunks and this item's output is the partial of chunk ch
+  struct Item { int4 tl[2]; int nk[2]; int nch[2]; int nkv, kv_base, kvh, c0, pr, ch; };
+  const bool chunked = a.chunk_per_cta > 0.f;
+  int* s_order = reinterpret_cast<int*>(smem + OFF_SCHED);  // [MAXP] pair of rank r
+  int* s_start = s_order + MAXP;                           // [MAXP + 1] first item of rank r
+  int* s_nkv = s_start + MAXP + 1;                         // [MAXP] KV tiles of pair p
+  int* s_nch = s_nkv + MAXP;                               // [MAXP] chunks of pair p
+  int* s_len = s_nch + MAXP;                               // [1] chunk length
+  volatile int* s_merge = s_len + 1;                       // [2] tile t: this CTA merges the partials
+  auto tile_nk = [&](const int4& tl) { return tl.y > 0 ? a.qpos[tl.x + tl.y - 1] / BKV + 1 : 0; };  // rows sorted by position
   auto decode = [&](int w) {
     Item it;
-    const int pr = n_pairs - 1 - w / a.n_kv_heads;
-    it.kvh = w % a.n_kv_heads;
+    int pr;
+    if (chunked) {
+      int lo = 0, hi = n_pairs - 1;  // largest rank whose first item is <= w
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_start[mid] <= w) lo = mid; else hi = mid - 1;
+      }
+      pr = s_order[lo];
+      const int local = w - s_start[lo];
+      it.ch = local / a.n_kv_heads;
+      it.kvh = local % a.n_kv_heads;
+    } else {
+      pr = n_pairs - 1 - w / a.n_kv_heads;
+      it.kvh = w % a.n_kv_heads;
+      it.ch = 0;
+    }
+    it.pr = pr;
+    int nkt[2];
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       it.tl[t] = a.tiles[2 * pr + t];
-      it.nk[t] = it.tl[t].y > 0 ? a.qpos[it.tl[t].x + it.tl[t].y - 1] / BKV + 1 : 0;  // rows sorted by position
+      nkt[t] = tile_nk(it.tl[t]);
     }
-    it.nkv = max(it.nk[0], it.nk[1]);
+    const int nkvp = max(nkt[0], nkt[1]);
+    const int nch = chunked ? s_nch[pr] : 1;
+    it.c0 = it.ch * nkvp / nch;
+    const int c1 = (it.ch + 1) * nkvp / nch;
+    it.nkv = c1 - it.c0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      it.nk[t] = max(0, min(c1, nkt[t]) - it.c0);
+      int n = 0;  // chunks that reach into tile t's range
+      for (int c = 0; c < nch; ++c) n += (c * nkvp / nch < nkt[t]) ? 1 : 0;
+      it.nch[t] = n;
+    }
     it.kv_base = it.tl[0].z;
     return it;
   };
+  auto tile_bar = [](int t) {  // the 4 softmax warps of tile t
+    if (t == 0) asm volatile("bar.sync 2, 128;" ::: "memory");
+    else asm volatile("bar.sync 3, 128;" ::: "memory");
+  };
+  if (chunked) {  // per-CTA schedule (identical in every CTA): pairs ranked by chunk length, longest first
+    if (warp == 0) {
+      int tot = 0;
+      for (int p = lane; p < n_pairs; p += 32) {
+        const int v = max(tile_nk(a.tiles[2 * p]), tile_nk(a.tiles[2 * p + 1]));
+        s_nkv[p] = v;
+        tot += v;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      const float target = static_cast<float>(tot) * a.n_kv_heads / (a.chunk_per_cta * gridDim.x);
+      const int len = max(2, static_cast<int>(ceilf(target)));
+      __syncwarp();
+      for (int p = lane; p < n_pairs; p += 32) {
+        const int v = s_nkv[p];
+        s_nch[p] = v == 0 ? 0 : min(ATTN_MAX_CHUNKS, (v + len - 1) / len);
+      }
+      __syncwarp();
+      for (int p = lane; p < n_pairs; p += 32) {  // rank: longer chunks first (v / nch), then higher pair
+        const int v = s_nkv[p], n = s_nch[p];
+        int rank = 0;
+        for (int q2 = 0; q2 < n_pairs; ++q2) {
+          const int vq = s_nkv[q2], nq = s_nch[q2];
+          // compare vq / nq with v / n (empty pairs: length -1, last)
+          const long long lq = nq ? static_cast<long long>(vq) * (n ? n : 1) : -1;
+          const long long lp = n ? static_cast<long long>(v) * (nq ? nq : 1) : -1;
+          rank += (lq > lp || (lq == lp && q2 > p)) ? 1 : 0;
+        }
+        s_order[rank] = p;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        int acc = 0;
+        for (int r = 0; r < n_pairs; ++r) { s_start[r] = acc; acc += s_nch[s_order[r]] * a.n_kv_heads; }
+        s_start[n_pairs] = acc;
+        *s_len = len;
+      }
+    }
+    __syncthreads();
+  }
+  const int n_items_all = chunked ? s_start[n_pairs] : n_items;
   // consumers: item i of this CTA (-1 = no more work); the slot is released right after the read
   auto next_item = [&](int i, bool warp_wide) {
     mbar_wait(&it_full[i & 1], (i >> 1) & 1);
@@ -138,7 +226,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int i = 0;; ++i) {
         if (i >= 2) mbar_wait(&it_empty[i & 1], ((i - 2) >> 1) & 1);
         int w = atomicAdd(a.work_ctr, 1);
-        if (w >= n_items) w = -1;
+        if (w >= n_items_all) w = -1;
         item_slot[i & 1] = w;
         mbar_arrive(&it_full[i & 1]);  // release: the slot write is visible to the waiters
         if (w < 0) break;
@@ -151,7 +239,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tma_load_3d(sQ + t * TILE, &tmQ, q_full, 0, it.kvh * G, it.tl[t].x);
           tma_load_3d(sQ + t * TILE + HALF, &tmQ, q_full, 64, it.kvh * G, it.tl[t].x);
         }
-        const int krow0 = static_cast<int>(it.kvh * t_cap + it.kv_base);
+        const int krow0 = static_cast<int>(it.kvh * t_cap + it.kv_base) + it.c0 * BKV;
         for (int j = 0; j < it.nkv; ++j, ++kc) {
           const int s = kc % KST;
           mbar_wait(&k_empty[s], ((kc / KST) & 1) ^ 1);
@@ -172,7 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int s = vc % VST;
           mbar_wait(&v_empty[s], ((vc / VST) & 1) ^ 1);
           v_rows_cp_async(sV + s * TILE, a.vsrc, a.v, a.head_stride,
-                          static_cast<int64_t>(it.kv_base) + static_cast<int64_t>(j) * BKV, it.kvh, t_cap);
+                          static_cast<int64_t>(it.kv_base) + static_cast<int64_t>(it.c0 + j) * BKV, it.kvh, t_cap);
           cp_async_mbar_arrive(&v_full[s]);  // arrives when this lane's copies land (no wait here)
         }
       }
@@ -183,7 +271,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int w = next_item(i, false);
         if (w < 0) break;
         const Item it = decode(w);
-        const int vrow0 = static_cast<int>(it.kvh * t_cap + it.kv_base);
+        const int vrow0 = static_cast<int>(it.kvh * t_cap + it.kv_base) + it.c0 * BKV;
         for (int j = 0; j < it.nkv; ++j, ++vc) {
           const int s = vc % VST;
           mbar_wait(&v_empty[s], ((vc / VST) & 1) ^ 1);
@@ -296,7 +384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tmem_ld32(s_col + hh * 64, sr);
           tmem_ld32(s_col + hh * 64 + 32, sr + 32);
           tmem_wait_ld();
-          const int key0 = j * BKV + hh * 64;
+          const int key0 = (it.c0 + j) * BKV + hh * 64;
           const bool full = key0 + 63 <= p_first;  // every row sees every key of the half: no causal mask
           uint32_t pk[32];
           // common case: exps against the running max, no row-max pass at all. Kept unless some row's sum
@@ -361,6 +449,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
       uint16_t* dst = a.o + static_cast<int64_t>(row_start + tt) * H * DH + (it.kvh * G + g) * DH;
+      const bool part = it.nch[t] > 1;  // KV-chunked tile: fp32 partial (O / l, m, l) of chunk it.ch
+      const int64_t slot0 = (static_cast<int64_t>(2 * it.pr + t) * a.n_kv_heads + it.kvh) * ATTN_MAX_CHUNKS;
+      float* pdst = part ? a.part_o + ((slot0 + it.ch) * ROWS + r) * DH : nullptr;
+      if (part) {
+        a.part_ml[((slot0 + it.ch) * ROWS + r) * 2] = m_run;
+        a.part_ml[((slot0 + it.ch) * ROWS + r) * 2 + 1] = l_run;
+      }
 #pragma unroll 1
       for (int c = 0; c < DH; c += 32) {
         uint32_t o[32];
@@ -371,7 +466,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&o_free[t]);
         }
-        if (valid) {
+        if (part) {
+#pragma unroll
+          for (int i2 = 0; i2 < 32; i2 += 4)
+            *reinterpret_cast<float4*>(pdst + c + i2) =
+                make_float4(__uint_as_float(o[i2]) * inv, __uint_as_float(o[i2 + 1]) * inv,
+                            __uint_as_float(o[i2 + 2]) * inv, __uint_as_float(o[i2 + 3]) * inv);
+        } else if (valid) {
 #pragma unroll
           for (int i2 = 0; i2 < 32; i2 += 8) {
             uint4 u;
@@ -380,6 +481,51 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             u.z = pack_bf2(__uint_as_float(o[i2 + 4]) * inv, __uint_as_float(o[i2 + 5]) * inv);
             u.w = pack_bf2(__uint_as_float(o[i2 + 6]) * inv, __uint_as_float(o[i2 + 7]) * inv);
             *reinterpret_cast<uint4*>(dst + c + i2) = u;
+          }
+        }
+      }
+      if (part) {  // arrival count per (tile, kv head); the chunk that arrives last merges and resets it
+        __threadfence();
+        tile_bar(t);
+        if (q == 0 && lane == 0) {
+          int* ctr = a.split_flag + (2 * it.pr + t) * a.n_kv_heads + it.kvh;
+          const bool last = atomicAdd(ctr, 1) == it.nch[t] - 1;
+          if (last) *ctr = 0;
+          s_merge[t] = last ? 1 : 0;
+        }
+        tile_bar(t);
+        if (s_merge[t] && valid) {
+          __threadfence();
+          float mm = -INFINITY;
+          for (int c2 = 0; c2 < it.nch[t]; ++c2) {
+            const float2 v = __ldcg(reinterpret_cast<const float2*>(a.part_ml + ((slot0 + c2) * ROWS + r) * 2));
+            if (v.y > 0.f) mm = fmaxf(mm, v.x);
+          }
+          float wts[ATTN_MAX_CHUNKS], wsum = 0.f;
+#pragma unroll
+          for (int c2 = 0; c2 < ATTN_MAX_CHUNKS; ++c2) {
+            wts[c2] = 0.f;
+            if (c2 >= it.nch[t]) continue;
+            const float2 v = __ldcg(reinterpret_cast<const float2*>(a.part_ml + ((slot0 + c2) * ROWS + r) * 2));
+            if (v.y > 0.f) wts[c2] = v.y * fast_exp2(v.x - mm);
+            wsum += wts[c2];
+          }
+          const float inv2 = wsum > 0.f ? 1.f / wsum : 0.f;
+#pragma unroll 1
+          for (int c = 0; c < DH; c += 8) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c2 = 0; c2 < ATTN_MAX_CHUNKS; ++c2) {
+              if (wts[c2] == 0.f) continue;
+              const float4* src = reinterpret_cast<const float4*>(a.part_o + ((slot0 + c2) * ROWS + r) * DH + c);
+              const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+              acc[0] += wts[c2] * x0.x; acc[1] += wts[c2] * x0.y; acc[2] += wts[c2] * x0.z; acc[3] += wts[c2] * x0.w;
+              acc[4] += wts[c2] * x1.x; acc[5] += wts[c2] * x1.y; acc[6] += wts[c2] * x1.z; acc[7] += wts[c2] * x1.w;
+            }
+            uint4 u;
+            u.x = pack_bf2(acc[0] * inv2, acc[1] * inv2); u.y = pack_bf2(acc[2] * inv2, acc[3] * inv2);
+            u.z = pack_bf2(acc[4] * inv2, acc[5] * inv2); u.w = pack_bf2(acc[6] * inv2, acc[7] * inv2);
+            *reinterpret_cast<uint4*>(dst + c) = u;
           }
         }
       }
@@ -404,6 +550,9 @@ cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, con
                              const AttnArgs& a, int64_t t_cap, cudaStream_t s) {
   if (a.n_tiles <= 0) return cudaSuccess;
   if (a.n_tiles % 2 != 0 || a.head_dim != DH || a.n_splits != 1) return cudaErrorInvalidValue;
+  const bool chunked = a.chunk_per_cta > 0.f;
+  if (chunked && (a.n_tiles / 2 > ATTN_CHUNK_MAX_PAIRS || !a.part_o || !a.part_ml || !a.split_flag))
+    return cudaErrorInvalidValue;
   if (cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_attn_pair), SMEM_BYTES); e != cudaSuccess) return e;
   if (a.work_ctr == nullptr) return cudaErrorInvalidValue;
   static const int sms = [] {
@@ -417,8 +566,26 @@ cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, con
     return !(e && atoi(e) == 0);
   }();
   const int items = a.n_tiles / 2 * a.n_kv_heads;
-  const int grid = persist ? (items < sms ? items : sms) : items;
+  // chunked: the item count is known on the device only (it follows the tiles' causal lengths)
+  const int grid = chunked ? sms : persist ? (items < sms ? items : sms) : items;
   return launch_pdl(k_attn_pair, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, *tmQ, *tmK, *tmV, a, t_cap);
+}
+
+bool attn_chunk_auto() {
+  static const bool on = [] {
+    const char* e = getenv("RC_ATTN_CHUNK_AUTO");  // 1 = AUTO takes the chunked launch for small grids
+    return e && atoi(e) == 1;
+  }();
+  return on;
+}
+
+float attn_chunk_per_cta() {
+  static const float f = [] {
+    const char* e = getenv("RC_ATTN_CHUNK_F");  // diagnostics: items per CTA the chunk length aims at
+    const float v = e ? static_cast<float>(atof(e)) : 2.0f;
+    return v > 0.f ? v : 2.0f;
+  }();
+  return f;
 }
 
 bool attn_use_pairs(int n_tiles, int n_kv_heads, int num_sms) {

@@ -38,6 +38,7 @@ constexpr int BM = 128, BK = 64;
 constexpr int WS_TILE = 128 * 256;  // floats of one workspace slot: [256 columns][128 lanes]
 // raster: group_m m-tiles share a sweep over n; the host sizes the group by the bytes of its A rows
 // (they must stay in L2 while the sweep streams B; B is re-read ceil(num_m / group_m) times).
+constexpr size_t GROUP_B_BYTES = size_t(56) << 20;  // n-grouped raster: B bands kept (evict_last) per group
 constexpr size_t GROUP_A_BYTES = size_t(32) << 20;  // measured: gate/up at cfg3 b32 3.14 -> 3.07 ms, DRAM 3.1 -> 1.9 GB vs 16 MB
 
 template <int BN>
@@ -149,7 +150,20 @@ __device__ __forceinline__ bool unit_at(const Sched& sc, int it, Unit& un) {
   return true;
 }
 
+// group_m < 0: the transposed raster, -group_m n-tiles share a sweep over m (B stays in L2, A is
+// re-read ceil(num_n / -group_m) times); the host picks the raster with the lower estimated traffic
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
+  if (group_m < 0) {
+    const int gn_max = -group_m;
+    const int per_group = gn_max * num_m;
+    const int g = t / per_group;
+    const int first_n = g * gn_max;
+    const int gn = min(gn_max, num_n - first_n);
+    const int r = t - g * per_group;
+    nb = first_n + r % gn;
+    mb = r / gn;
+    return;
+  }
   const int per_group = group_m * num_n;
   const int g = t / per_group;
   const int first_m = g * group_m;
@@ -658,6 +672,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
       Unit un;
+      // n-grouped raster: B resident across the group's waves, A streamed
+      const bool hint = group_m < 0;
+      const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
         const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
@@ -665,8 +682,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
           if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
-          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow);
-          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
+          if (hint) {
+            tma_load_2d_pair_hint(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow, pol_a);
+            tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow, pol_b);
+          } else {
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1039,8 +1061,24 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
     const char* e = std::getenv("RC_GROUP_A_MB");
     return e ? static_cast<size_t>(std::atoi(e)) << 20 : GROUP_A_BYTES;
   }();
-  const int group_m = static_cast<int>(std::max<size_t>(
+  int group_m = static_cast<int>(std::max<size_t>(
       2, std::min<size_t>(num_m, group_a_bytes / (static_cast<size_t>(2 * BM) * K * 2))));
+  {  // raster by estimated DRAM traffic: m-groups re-read B once per group, n-groups re-read A
+    // default m-groups: the n-grouped raster with evict_last B / evict_first A measured slower at cfg3
+    // batch 32 (GEMMs 250.7 -> 261.5 ms per step) and raised the gate/up DRAM bytes 2.43 -> 5.74 GB per
+    // launch (A lines evicted before the group's other n-tiles read them)
+    static const int raster = [] { const char* e = std::getenv("RC_GEMM_RASTER"); return e ? std::atoi(e) : 0; }();
+    static const size_t group_b_bytes = [] {
+      const char* e = std::getenv("RC_GROUP_B_MB");
+      return e ? static_cast<size_t>(std::atoi(e)) << 20 : GROUP_B_BYTES;
+    }();
+    const int num_n = (N + 255) / 256;
+    const double band = 256.0 * K * 2;  // bytes of one 256-row band of A or B
+    const int gn = static_cast<int>(std::max<size_t>(1, std::min<size_t>(num_n, group_b_bytes / static_cast<size_t>(band))));
+    const double tm = band * (num_m + num_n * double((num_m + group_m - 1) / group_m));
+    const double tn = band * (num_n + num_m * double((num_n + gn - 1) / gn));
+    if (raster == 1 || (raster == -1 && tn < 0.8 * tm)) group_m = -gn;
+  }
   return launch_pdl(k_gemm_pair<EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits,
                     group_m, sk_tiles, ep);
 }
@@ -1177,7 +1215,9 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   // CTA pairs for 256-wide GEMMs with M >= 1024: at cfg3 batch 32 they lift the GEMMs from 0.92 to
   // 0.99 of the measured sustained peak. RC_GEMM_PAIR=0/1 forces.
   static const int pair_mode = [] { const char* e = std::getenv("RC_GEMM_PAIR"); return e ? std::atoi(e) : -1; }();
-  const bool pair = pair_mode == 1 || (pair_mode == -1 && (M >= 1024 || (epi == EPI_ADD_F32 && M > 2 * BM)));
+  // RC_GEMM_PAIR_MIN_M: the M from which the non-residual epilogues take CTA pairs (diagnostics)
+  static const int pair_min_m = [] { const char* e = std::getenv("RC_GEMM_PAIR_MIN_M"); return e ? std::atoi(e) : 1024; }();
+  const bool pair = pair_mode == 1 || (pair_mode == -1 && (M >= pair_min_m || (epi == EPI_ADD_F32 && M > 2 * BM)));
   if (pair && bn == 256 && M > BM && num_sms >= 2) {
     switch (epi) {
       case EPI_BF16: return launch_pair<EPI_BF16>(a, b, c, M, N, K, ep, num_sms, s);

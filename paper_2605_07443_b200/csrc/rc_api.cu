@@ -1097,7 +1097,7 @@ rc_status run_qkv(rc_ctx* c, int l, float* x, int32_t rows, const int32_t* d_pos
 // second half: attention of the `rows` query rows (q in c->q, positions d_pos) over the arena,
 // O-projection + residual, RMSNorm, SwiGLU MLP + residual
 rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
-                   const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min, bool paired,
+                   const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min, int paired,
                    double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
   const rc_model_desc& m = c->m;
   const int d = m.d_model, dh = m.head_dim, H = m.n_heads, Hk = m.n_kv_heads, F = m.d_ff;
@@ -1112,8 +1112,9 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
   at.debug_mode = attn_debug;
   at.n_splits = n_splits;
   at.split_min = split_min;
-  if (n_splits > 1) {  // partial-output workspace, grown on first use
-    const size_t need = static_cast<size_t>(n_tiles) * Hk * 128;
+  if (paired == 2) at.chunk_per_cta = attn_chunk_per_cta();
+  if (n_splits > 1 || paired == 2) {  // partial-output workspace, grown on first use
+    const size_t need = static_cast<size_t>(n_tiles) * Hk * 128 * (paired == 2 ? ATTN_MAX_CHUNKS : 1);
     if (c->part_rows < need) {
       if (c->part_o) cudaFree(c->part_o);
       if (c->part_ml) cudaFree(c->part_ml);
@@ -1121,8 +1122,9 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
       cudaError_t e;
       c->part_o = dev_alloc<float>(need * 128, &e);
       if (e == cudaSuccess) c->part_ml = dev_alloc<float>(need * 2, &e);
-      if (e == cudaSuccess) c->part_flag = dev_alloc<int32_t>(static_cast<size_t>(n_tiles) * Hk, &e);
-      if (e == cudaSuccess) e = cudaMemset(c->part_flag, 0, static_cast<size_t>(n_tiles) * Hk * sizeof(int32_t));
+      // arrival counters per (tile, kv head): need / 128 >= n_tiles * Hk for every later launch that fits
+      if (e == cudaSuccess) c->part_flag = dev_alloc<int32_t>(need / 128, &e);
+      if (e == cudaSuccess) e = cudaMemset(c->part_flag, 0, need / 128 * sizeof(int32_t));
       if (e != cudaSuccess) { c->part_rows = 0; return fail(RC_E_NOMEM, "attention split workspace"); }
       c->part_rows = need;
     }
@@ -1167,7 +1169,7 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
 // one decoder layer over `rows` query rows (U or Sel) -- a2 / a5-a7
 rc_status run_layer(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t rows, const int32_t* d_pos,
                     const int32_t* d_dst, const int4* d_tiles, int32_t n_tiles, int32_t n_splits, int32_t split_min,
-                    bool paired, double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
+                    int paired, double attn_flops, int attn_pending, int det, bool zc_layer, cudaStream_t s) {
   rc_status st = run_qkv(c, l, x, rows, d_pos, d_dst, nullptr, s);
   if (st != RC_OK) return st;
   return run_rest(c, l, x, mx, rows, d_pos, d_tiles, n_tiles, n_splits, split_min, paired, attn_flops, attn_pending,
@@ -1281,7 +1283,7 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   for (auto& p : plan) { n_ut += ntiles(p.u_cnt); n_st += ntiles(p.sel_cnt); }
   // small grids (e.g. one request's selected rows) fill the SMs badly: split the KV range of every
   // query tile over several CTAs and merge (tcgen05 kernel only); every entry repeats per split
-  if (prm->attn_kernel < RC_ATTN_AUTO || prm->attn_kernel > RC_ATTN_ADAPTIVE)
+  if (prm->attn_kernel < RC_ATTN_AUTO || prm->attn_kernel > RC_ATTN_CHUNKED)
     return fail(RC_E_INVALID, "attn_kernel must be one of RC_ATTN_*");
   const int ak = c->attn_tc ? prm->attn_kernel : RC_ATTN_SINGLE;
   int split_u = 1, split_s = 1, smin_u = 0, smin_s = 0;
@@ -1304,10 +1306,18 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   }
   // large grids: two query tiles of one request per CTA share every K/V tile load (k_attn_pair.cu);
   // a request's odd tile count is padded with one empty tile
-  bool pair_u = false, pair_s = false;
-  if (c->attn_tc && m.head_dim == 128 && (ak == RC_ATTN_AUTO || ak == RC_ATTN_PAIRED)) {
-    pair_u = split_u == 1 && (ak == RC_ATTN_PAIRED || attn_use_pairs(n_ut, m.n_kv_heads, c->num_sms));
-    pair_s = split_s == 1 && (ak == RC_ATTN_PAIRED || attn_use_pairs(n_st, m.n_kv_heads, c->num_sms));
+  // (2 = the same kernel with device-sized KV chunks, for grids too small for plain pairs)
+  int pair_u = 0, pair_s = 0;
+  if (c->attn_tc && m.head_dim == 128 && (ak == RC_ATTN_AUTO || ak == RC_ATTN_PAIRED || ak == RC_ATTN_CHUNKED)) {
+    auto mode = [&](int n_tiles, int split) {
+      if (split != 1) return 0;
+      if (ak == RC_ATTN_PAIRED || (ak == RC_ATTN_AUTO && attn_use_pairs(n_tiles, m.n_kv_heads, c->num_sms))) return 1;
+      const int pairs_bound = n_tiles / 2 + n_req;  // padded pair count
+      if (pairs_bound > ATTN_CHUNK_MAX_PAIRS) return ak == RC_ATTN_CHUNKED ? 1 : 0;
+      return (ak == RC_ATTN_CHUNKED || (ak == RC_ATTN_AUTO && attn_chunk_auto())) ? 2 : 0;
+    };
+    pair_u = mode(n_ut, split_u);
+    pair_s = mode(n_st, split_s);
     auto padded = [&](bool u) {
       int32_t n = 0;
       for (auto& p : plan) n += (ntiles(u ? p.u_cnt : p.sel_cnt) + 1) / 2 * 2;

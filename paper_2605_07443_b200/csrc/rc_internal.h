@@ -187,6 +187,10 @@ struct AttnArgs {
   int32_t split_min = 0;     // > 0 with n_splits = 2: adaptive split (tiles under split_min KV tiles unsplit)
   int32_t* split_flag = nullptr;  // [n_tiles / n_splits][Hk]: split CTAs' arrival counters (zero between launches)
   int32_t* work_ctr = nullptr;    // paired kernel: {next work item, finished CTAs}, zero between launches
+  // paired kernel, KV chunks (small grids): > 0 cuts every pair's KV range into chunks of about
+  // (all pair-steps) / (chunk_per_cta * grid) KV tiles; partials per chunk in part_o / part_ml at slot
+  // ((tile * Hk + kvh) * ATTN_MAX_CHUNKS + chunk), merged by the last-arriving chunk (split_flag)
+  float chunk_per_cta = 0.f;
   VSrc vsrc;                      // zero-copy V: V rows through vmap (cp.async loads) instead of TMA boxes
 };
 int attn_tokens_per_tile(int group);
@@ -202,6 +206,10 @@ cudaError_t attn_tc_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const
 cudaError_t attn_pair_launch(const CUtensorMap* tmQ, const CUtensorMap* tmK, const CUtensorMap* tmV,
                              const AttnArgs& a, int64_t t_cap, cudaStream_t s);
 bool attn_use_pairs(int n_tiles, int n_kv_heads, int num_sms);
+// KV-chunked paired launch (a.chunk_per_cta > 0): at most this many pairs, chunks per pair
+constexpr int ATTN_CHUNK_MAX_PAIRS = 128, ATTN_MAX_CHUNKS = 8;
+bool attn_chunk_auto();        // AUTO picks the chunked launch for small grids (RC_ATTN_CHUNK_AUTO)
+float attn_chunk_per_cta();    // items per CTA the chunk length aims at (RC_ATTN_CHUNK_F)
 // NEXT-1 attention mass (k_attn_mass.cu): column sums of the check-layer softmax per key
 struct MassArgs {
   const int4* key_tiles;  // {request, first key position, keys in tile (<= 128), 0}

@@ -322,13 +322,13 @@ def test_ragged_batch_matches_per_request():
 
 
 @pytest.mark.parametrize("wl", [rcgen.MINI_L, rcgen.MINI_Q])
-@pytest.mark.parametrize("attn_kernel", [1, 2, 3, 4])
+@pytest.mark.parametrize("attn_kernel", [1, 2, 3, 4, 5])
 def test_attention_launch_shapes_match_oracle(wl, attn_kernel):
     """Every attention launch shape (one query tile per CTA, two tiles of one request per CTA with
-    an odd tile count padded, KV split + merge, adaptive split) on a ragged 3-request batch, layers < c
-    included."""
+    an odd tile count padded, KV split + merge, adaptive split, persistent pairs with device-sized KV
+    chunks merged by the last chunk) on a ragged 3-request batch, layers < c included."""
     from paper_2605_07443_b200 import _lib as R
-    assert (R.RC_ATTN_SINGLE, R.RC_ATTN_PAIRED, R.RC_ATTN_SPLIT2, R.RC_ATTN_ADAPTIVE) == (1, 2, 3, 4)
+    assert (R.RC_ATTN_SINGLE, R.RC_ATTN_PAIRED, R.RC_ATTN_SPLIT2, R.RC_ATTN_ADAPTIVE, R.RC_ATTN_CHUNKED) == (1, 2, 3, 4, 5)
     case = make_case(wl, n_req=3)
     pools = oracle_pools(case)
     res, lays = _run_gpu(wl, case, pools, 1500, attn_kernel=attn_kernel)
