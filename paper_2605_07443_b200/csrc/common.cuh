@@ -254,6 +254,13 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* map, uin
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster_addr), "r"(c0), "r"(c1)
       : "memory");
 }
+// L2 prefetch of one TMA box (no shared-memory destination, no completion): streaming operands that
+// come from HBM are requested k-blocks ahead of their real loads
+__device__ __forceinline__ void tma_prefetch_l2_2d(const void* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 // the same with an L2 eviction-priority policy (createpolicy): the operand a raster keeps resident
 // across waves loads evict_last, the one it streams evict_first
 __device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const void* map, uint32_t bar_cluster_addr, int c0, int c1,

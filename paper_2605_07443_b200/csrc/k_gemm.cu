@@ -150,6 +150,37 @@ __device__ __forceinline__ bool unit_at(const Sched& sc, int it, Unit& un) {
   return true;
 }
 
+// ------------------------------------------------------------------ weight prefetch
+// The weight operand of a small-M GEMM streams from HBM once (batch 1: 436 MB per layer), so every
+// k-block's TMA load pays the HBM latency, which a 4-6 stage ring does not cover. The producer keeps
+// an L2 prefetch PF k-blocks ahead of its loads over its whole unit sequence (unit boundaries
+// included), and issues the first PF before griddepcontrol.wait: weights are never written by the
+// previous kernel, so they load while it drains. RC_GEMM_PF = distance in k-blocks (0 = off).
+int gemm_pf_distance() {
+  // default off: measured slower at both batch sizes (cfg3 b1 11.7 -> 12.7 ms, b32 287 -> 309 ms at
+  // distance 8; distances 4 and 16 alike): the prefetch issue itself costs the producer thread
+  static const int pf = [] { const char* e = std::getenv("RC_GEMM_PF"); return e ? std::atoi(e) : 0; }();
+  return pf;
+}
+template <class At>
+struct PfCursor {  // (unit, k-block) sequence of one producer; At(it, un, row) -> bool, row = weight row
+  At at;
+  int it = 0, kb = 0, kb1 = 0, row = 0;
+  bool ok = false;
+  __device__ __forceinline__ void start() {
+    Unit un;
+    ok = at(0, un, row);
+    kb = un.kb0; kb1 = un.kb1;
+  }
+  __device__ __forceinline__ void next() {
+    if (!ok) return;
+    if (++kb < kb1) return;
+    Unit un;
+    ok = at(++it, un, row);
+    kb = un.kb0; kb1 = un.kb1;
+  }
+};
+
 // group_m < 0: the transposed raster, -group_m n-tiles share a sweep over m (B stays in L2, A is
 // re-read ceil(num_n / -group_m) times); the host picks the raster with the lower estimated traffic
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
@@ -544,8 +575,6 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
-  griddep_launch();
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
@@ -553,6 +582,25 @@ __global__ void __launch_bounds__(256, 1)
   const int units = tiles * splits;
   Sched sc{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), units, splits, num_m, num_n, group_m, BM, 0};
   sc.nk = nk;
+  auto w_at = [&](int it, Unit& un, int& row) {
+    if (!unit_at(sc, it, un)) return false;
+    int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
+    row = nb * BN;
+    return true;
+  };
+  PfCursor<decltype(w_at)> pfc{w_at};
+  auto pf_issue = [&]() {  // the weight boxes of the cursor's k-block, then advance
+    if (!pfc.ok) return;
+#pragma unroll
+    for (int h = 0; h < BN / 128; ++h) tma_prefetch_l2_2d(&tmB, pfc.kb * BK, pfc.row + h * 128);
+    pfc.next();
+  };
+  if (warp == 0 && lane == 0 && ep.pf > 0) {  // weights only: safe before the PDL wait
+    pfc.start();
+    for (int i = 0; i < ep.pf; ++i) pf_issue();
+  }
+  griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
@@ -561,6 +609,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
+          if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
@@ -655,8 +704,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();  // barrier inits and both TMEM allocations visible pair-wide
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  griddep_wait();
-  griddep_launch();
 
   const int num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
@@ -667,6 +714,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   Sched sc{cid, ncl, units, splits, num_m, num_n, group_m, 2 * BM, static_cast<int>(rank) * BM};
   sc.nk = nk;
   sc.sk_tiles = sk_tiles;
+  auto w_at = [&](int it, Unit& un, int& row) {
+    if (!unit_at(sc, it, un)) return false;
+    int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
+    row = nb * BN + static_cast<int>(rank) * 128;  // this CTA's 128 weight rows
+    return true;
+  };
+  PfCursor<decltype(w_at)> pfc{w_at};
+  auto pf_issue = [&]() {
+    if (!pfc.ok) return;
+    tma_prefetch_l2_2d(&tmB, pfc.kb * BK, pfc.row);
+    pfc.next();
+  };
+  if (warp == 0 && lane == 0 && ep.pf > 0) {  // weights only: safe before the PDL wait
+    pfc.start();
+    for (int i = 0; i < ep.pf; ++i) pf_issue();
+  }
+  griddep_wait();
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
@@ -679,6 +744,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
         const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
+          if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
           if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
@@ -919,12 +985,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  griddep_wait();
-  griddep_launch();
 
   const int nfull = M / 256, rem = M - nfull * 256;
   const TSched sc{static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), N / 256, nfull,
                   rem > 0 ? (rem <= 128 ? 128 : 256) : 0, splits, (K + BK - 1) / BK};
+  auto w_at = [&](int it, Unit& un, int& row) {
+    int s, t0, ncols;
+    if (!sc.at(it, s, t0, ncols, un)) return false;
+    row = s * 256 + static_cast<int>(rank) * 128;  // this CTA's 128 weight rows
+    return true;
+  };
+  PfCursor<decltype(w_at)> pfc{w_at};
+  auto pf_issue = [&]() {
+    if (!pfc.ok) return;
+    tma_prefetch_l2_2d(&tmW, pfc.kb * BK, pfc.row);
+    pfc.next();
+  };
+  if (warp == 0 && lane == 0 && ep.pf > 0) {  // weights only: safe before the PDL wait
+    pfc.start();
+    for (int i = 0; i < ep.pf; ++i) pf_issue();
+  }
+  griddep_wait();
+  griddep_launch();
   const uint32_t leader_full = mapa_shared(full, 0);
   const uint32_t leader_tempty = mapa_shared(tempty, 0);
 
@@ -938,6 +1020,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const int half = ncols / 2;
         const int trow = t0 + rank * half;
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
+          if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
           if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2));
@@ -1201,8 +1284,10 @@ bool gemm_use_transposed(int M, int N, int epi, int head_dim, int num_sms) {
 }
 
 cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K, int bn,
-                        int epi, const EpiArgs& ep, int num_sms, cudaStream_t s, const CUtensorMap* a64) {
+                        int epi, const EpiArgs& ep_in, int num_sms, cudaStream_t s, const CUtensorMap* a64) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  EpiArgs ep = ep_in;
+  ep.pf = gemm_pf_distance();
   // small M (one request's selected rows): the transposed pair kernel keeps every 256-row MMA full
   if (a64 != nullptr && bn == 256 && gemm_use_transposed(M, N, epi, ep.head_dim, num_sms)) {
     switch (epi) {

@@ -94,6 +94,7 @@ struct EpiArgs {
   int* ws_cnt = nullptr;    // 2 * gemm_ws_slots()
   int32_t ws_slots = 0;
   int32_t det = 1;          // 0: partial tiles reduce-add straight into x in arrival order
+  int32_t pf = 0;           // weight L2-prefetch distance in k-blocks (set by gemm_launch)
 };
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
