@@ -45,6 +45,8 @@ def parse():
                     help="gradual filtering steps g (reading R-GF, NEXT-1 variant): Sel shrinks from --r-start at "
                          "the check layer to r at layer c + g; 0 = one-shot selection (default)")
     ap.add_argument("--r-start", type=int, default=0, help="gradual: ratio (bp) at the check layer")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="rc_prefill_params.deterministic = 1: every layer's split-K partials summed in K order")
     ap.add_argument("--attn-kernel", type=int, default=0,
                     help="rc_prefill_params.attn_kernel (RC_ATTN_*): 0 = AUTO (default); others for A/B runs")
     ap.add_argument("--distinct-batches", type=int, default=2)
@@ -115,11 +117,13 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- workload setup
 def gradual_kw(args, r_bp):
-    """selective_prefill keyword arguments of the gradual-filtering variant (R-GF), {} when off."""
+    """selective_prefill keyword arguments of the gradual-filtering variant (R-GF) and of the
+    deterministic mode (--deterministic), {} when both are off."""
+    kw = {"deterministic": True} if args.deterministic else {}
     if not args.gradual:
-        return {}
+        return kw
     r0 = max(args.r_start, r_bp)
-    return {"gradual": args.gradual, "r_start_rev_bp": r0, "r_start_item_bp": r0}
+    return dict(kw, gradual=args.gradual, r_start_rev_bp=r0, r_start_item_bp=r0)
 
 
 def shard_setup(wl, cat, protos, world, rank, batch, n_batches):
@@ -613,6 +617,7 @@ def run_ours(args, wl):
                       "lambda": args.lam,
                       **({"gradual": {"layers": args.gradual, "r_start": max(args.r_start, r_bp) / 1e4}}
                          if args.gradual else {}),
+                      **({"deterministic": True} if args.deterministic else {}),
                       "parallelism": (f"dp{world}: Alg. 1 sharded item pool, Eq. 2 routing, NVLink fetch"
                                       if world > 1 else "dp1"),
                       "l2": "inputs larger than L2 (16 GB weights + item pool per GPU)",

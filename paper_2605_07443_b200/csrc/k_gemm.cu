@@ -599,23 +599,42 @@ __global__ void __launch_bounds__(256, 1)
     pfc.start();
     for (int i = 0; i < ep.pf; ++i) pf_issue();
   }
+  // head loads: the weight boxes of the first k-blocks go into their (still free) stages before the
+  // PDL wait (weights are never produced by the previous kernel); their A boxes follow after it
+  int pre = 0;
+  if (warp == 0 && lane == 0 && ep.head > 0) {
+    Unit u0;
+    if (unit_at(sc, 0, u0)) {
+      int mb, nb; tile_coords(u0.tile, num_m, num_n, group_m, mb, nb);
+      const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
+      for (; pre < n; ++pre) {
+        mbar_expect_tx(&full[pre], C::A_BYTES + C::B_BYTES);
+#pragma unroll
+        for (int h = 0; h < BN / 128; ++h)
+          tma_load_2d(sB + pre * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[pre], (u0.kb0 + pre) * BK, nb * BN + h * 128);
+      }
+    }
+  }
   griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
   griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
-      int stage = 0; uint32_t phase = 0;
+      int stage = 0; uint32_t phase = 0, g = 0;
       Unit un;
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb, ++g) {
           if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          const bool head = g < static_cast<uint32_t>(pre);
+          if (!head) mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
+          if (!head) {
 #pragma unroll
-          for (int h = 0; h < BN / 128; ++h)  // B boxes are 128 rows (shared with the CTA-pair kernel)
-            tma_load_2d(sB + stage * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[stage], kb * BK, nb * BN + h * 128);
+            for (int h = 0; h < BN / 128; ++h)  // B boxes are 128 rows (shared with the CTA-pair kernel)
+              tma_load_2d(sB + stage * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[stage], kb * BK, nb * BN + h * 128);
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -730,6 +749,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     pfc.start();
     for (int i = 0; i < ep.pf; ++i) pf_issue();
   }
+  int pre = 0;  // head loads (see k_gemm): this CTA's weight half of the first k-blocks before the wait
+  if (warp == 0 && lane == 0 && ep.head > 0) {
+    Unit u0;
+    if (unit_at(sc, 0, u0)) {
+      int mb, nb; tile_coords(u0.tile, num_m, num_n, group_m, mb, nb);
+      const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
+      for (; pre < n; ++pre) {
+        if (leader) mbar_expect_tx(&full[pre], 2 * (C::A_BYTES + C::B_BYTES));
+        tma_load_2d_pair(sB + pre * C::B_BYTES, &tmB, leader_full + pre * 8, (u0.kb0 + pre) * BK,
+                         nb * BN + static_cast<int>(rank) * 128);
+      }
+    }
+  }
   griddep_wait();
   griddep_launch();
 
@@ -740,20 +772,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // n-grouped raster: B resident across the group's waves, A streamed
       const bool hint = group_m < 0;
       const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
+      uint32_t g = 0;
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
         const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb, ++g) {
           if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
-          if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          const bool head = g < static_cast<uint32_t>(pre);
+          if (leader && !head) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
           if (hint) {
             tma_load_2d_pair_hint(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow, pol_a);
-            tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow, pol_b);
+            if (!head) tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow, pol_b);
           } else {
             tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow);
-            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
+            if (!head) tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1005,26 +1039,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     pfc.start();
     for (int i = 0; i < ep.pf; ++i) pf_issue();
   }
-  griddep_wait();
-  griddep_launch();
   const uint32_t leader_full = mapa_shared(full, 0);
   const uint32_t leader_tempty = mapa_shared(tempty, 0);
+  int pre = 0;  // head loads (see k_gemm): this CTA's weight rows of the first k-blocks before the wait
+  if (warp == 0 && lane == 0 && ep.head > 0) {
+    int s0, t00, nc0;
+    Unit u0;
+    if (sc.at(0, s0, t00, nc0, u0)) {
+      const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
+      for (; pre < n; ++pre) {
+        if (leader) mbar_expect_tx(&full[pre], 2 * (C::A_BYTES + static_cast<uint32_t>(nc0 / 2) * BK * 2));
+        tma_load_2d_pair(sA + pre * C::A_BYTES, &tmW, leader_full + pre * 8, (u0.kb0 + pre) * BK,
+                         s0 * 256 + static_cast<int>(rank) * 128);
+      }
+    }
+  }
+  griddep_wait();
+  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-      int stage = 0; uint32_t phase = 0;
+      int stage = 0; uint32_t phase = 0, g = 0;
       int s, t0, ncols;
       Unit un;
       for (int it = 0; sc.at(it, s, t0, ncols, un); ++it) {
         const int wrow = s * 256 + rank * 128;
         const int half = ncols / 2;
         const int trow = t0 + rank * half;
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb, ++g) {
           if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
-          if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2));
-          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmW, fb, kb * BK, wrow);
+          const bool head = g < static_cast<uint32_t>(pre);
+          if (leader && !head) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2));
+          if (!head) tma_load_2d_pair(sA + stage * C::A_BYTES, &tmW, fb, kb * BK, wrow);
           // one box per CTA: 128 token rows (full tile) or 64 (tail); the TMA issue count matters (four
           // 32-row boxes per full tile measured 12 % slower than two 64-row boxes at cfg3 batch 1)
           tma_load_2d_pair(sB + stage * C::B_BYTES, half == 128 ? &tmX128 : &tmX64, fb, kb * BK, trow);
@@ -1071,7 +1119,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * 256;
-      if constexpr (EPI == EPI_ADD_F32) {
+      if (ep.no_epi) {  // diagnostics (RC_GEMM_NOEPI=1): main loop only, the output is not written
+      } else if constexpr (EPI == EPI_ADD_F32) {
         epilogue_add<true>(taddr, ncols, f0 + q * 32, t0, q, &tmC, sOut, chunk_ctr, un, static_cast<int>(rank), ep,
                            s_flag);
       } else if constexpr (EPI == EPI_SWIGLU) {
@@ -1288,6 +1337,12 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   if (M <= 0 || N <= 0) return cudaSuccess;
   EpiArgs ep = ep_in;
   ep.pf = gemm_pf_distance();
+  // head loads (weights of the first k-blocks before the PDL wait): parity-green, within noise at cfg3
+  // batch 1 (11.89 / 11.92 / 12.04 vs 11.89 / 11.81 / 11.80 ms) and batch 32 (290.9 vs 290.9 ms): off
+  static const int head = [] { const char* e = std::getenv("RC_GEMM_HEAD"); return e ? std::atoi(e) : 0; }();
+  ep.head = head;
+  static const int no_epi = [] { const char* e = std::getenv("RC_GEMM_NOEPI"); return e ? std::atoi(e) : 0; }();
+  ep.no_epi = no_epi;
   // small M (one request's selected rows): the transposed pair kernel keeps every 256-row MMA full
   if (a64 != nullptr && bn == 256 && gemm_use_transposed(M, N, epi, ep.head_dim, num_sms)) {
     switch (epi) {

@@ -95,6 +95,8 @@ struct EpiArgs {
   int32_t ws_slots = 0;
   int32_t det = 1;          // 0: partial tiles reduce-add straight into x in arrival order
   int32_t pf = 0;           // weight L2-prefetch distance in k-blocks (set by gemm_launch)
+  int32_t head = 0;         // k-blocks whose weight boxes load before the PDL wait (set by gemm_launch)
+  int32_t no_epi = 0;       // diagnostics: transposed kernel skips its epilogue (RC_GEMM_NOEPI)
 };
 
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld_elems,
