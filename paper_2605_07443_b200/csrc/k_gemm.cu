@@ -181,6 +181,22 @@ struct PfCursor {  // (unit, k-block) sequence of one producer; At(it, un, row) 
   }
 };
 
+// k-block rotation (small M): CTAs that share an operand tile in the same wave all start its K loop
+// at k-block 0, so every k-block of the shared tile is requested by tens of SMs at once (at batch 1 the
+// 625 token rows are shared by every weight tile in flight). A unit whose weight tile index is `key`
+// walks its K range starting at (key % 16) / 16 of the way in, so the CTAs sharing a weight tile stay in
+// step (one HBM read) while those sharing the token tile are spread over 16 phases.
+__device__ __forceinline__ int kb_rot(const Unit& un, int key, int on) {
+  const int n = un.kb1 - un.kb0;
+  return on ? ((key & 15) * n) >> 4 : 0;
+}
+__device__ __forceinline__ int kb_at(const Unit& un, int i, int r) {
+  const int n = un.kb1 - un.kb0;
+  int j = i + r;
+  if (j >= n) j -= n;
+  return un.kb0 + j;
+}
+
 // group_m < 0: the transposed raster, -group_m n-tiles share a sweep over m (B stays in L2, A is
 // re-read ceil(num_n / -group_m) times); the host picks the raster with the lower estimated traffic
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
@@ -607,11 +623,12 @@ __global__ void __launch_bounds__(256, 1)
     if (unit_at(sc, 0, u0)) {
       int mb, nb; tile_coords(u0.tile, num_m, num_n, group_m, mb, nb);
       const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
+      const int rot = kb_rot(u0, nb, ep.krot);
       for (; pre < n; ++pre) {
         mbar_expect_tx(&full[pre], C::A_BYTES + C::B_BYTES);
 #pragma unroll
         for (int h = 0; h < BN / 128; ++h)
-          tma_load_2d(sB + pre * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[pre], (u0.kb0 + pre) * BK, nb * BN + h * 128);
+          tma_load_2d(sB + pre * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[pre], kb_at(u0, pre, rot) * BK, nb * BN + h * 128);
       }
     }
   }
@@ -624,7 +641,9 @@ __global__ void __launch_bounds__(256, 1)
       Unit un;
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
-        for (int kb = un.kb0; kb < un.kb1; ++kb, ++g) {
+        const int rot = kb_rot(un, nb, ep.krot);
+        for (int i = 0; i < un.kb1 - un.kb0; ++i, ++g) {
+          const int kb = kb_at(un, i, rot);
           if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const bool head = g < static_cast<uint32_t>(pre);
@@ -649,14 +668,14 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int i = 0; i < un.kb1 - un.kb0; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
+            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (i != 0 || k != 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -755,9 +774,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     if (unit_at(sc, 0, u0)) {
       int mb, nb; tile_coords(u0.tile, num_m, num_n, group_m, mb, nb);
       const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
+      const int rot = kb_rot(u0, nb, ep.krot);
       for (; pre < n; ++pre) {
         if (leader) mbar_expect_tx(&full[pre], 2 * (C::A_BYTES + C::B_BYTES));
-        tma_load_2d_pair(sB + pre * C::B_BYTES, &tmB, leader_full + pre * 8, (u0.kb0 + pre) * BK,
+        tma_load_2d_pair(sB + pre * C::B_BYTES, &tmB, leader_full + pre * 8, kb_at(u0, pre, rot) * BK,
                          nb * BN + static_cast<int>(rank) * 128);
       }
     }
@@ -770,13 +790,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int stage = 0; uint32_t phase = 0;
       Unit un;
       // n-grouped raster: B resident across the group's waves, A streamed
-      const bool hint = group_m < 0;
+      const bool hint = group_m < 0 && ep.hint;
       const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
       uint32_t g = 0;
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
         const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
-        for (int kb = un.kb0; kb < un.kb1; ++kb, ++g) {
+        const int rot = kb_rot(un, nb, ep.krot);
+        for (int i = 0; i < un.kb1 - un.kb0; ++i, ++g) {
+          const int kb = kb_at(un, i, rot);
           if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
@@ -803,14 +825,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int i = 0; i < un.kb1 - un.kb0; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (i != 0 || k != 0) ? 1u : 0u);
           umma_commit_pair(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1047,9 +1069,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     Unit u0;
     if (sc.at(0, s0, t00, nc0, u0)) {
       const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
+      const int rot = kb_rot(u0, s0, ep.krot);
       for (; pre < n; ++pre) {
         if (leader) mbar_expect_tx(&full[pre], 2 * (C::A_BYTES + static_cast<uint32_t>(nc0 / 2) * BK * 2));
-        tma_load_2d_pair(sA + pre * C::A_BYTES, &tmW, leader_full + pre * 8, (u0.kb0 + pre) * BK,
+        tma_load_2d_pair(sA + pre * C::A_BYTES, &tmW, leader_full + pre * 8, kb_at(u0, pre, rot) * BK,
                          s0 * 256 + static_cast<int>(rank) * 128);
       }
     }
@@ -1066,7 +1089,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const int wrow = s * 256 + rank * 128;
         const int half = ncols / 2;
         const int trow = t0 + rank * half;
-        for (int kb = un.kb0; kb < un.kb1; ++kb, ++g) {
+        const int rot = kb_rot(un, s, ep.krot);
+        for (int i = 0; i < un.kb1 - un.kb0; ++i, ++g) {
+          const int kb = kb_at(un, i, rot);
           if (ep.pf > 0) pf_issue();
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
@@ -1091,14 +1116,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         tc_fence_after();
         const uint32_t idesc = idesc_bf16_f32(256, ncols);
         const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int kb = un.kb0; kb < un.kb1; ++kb) {
+        for (int i = 0; i < un.kb1 - un.kb0; ++i) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (i != 0 || k != 0) ? 1u : 0u);
           umma_commit_pair(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1341,8 +1366,16 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   // batch 1 (11.89 / 11.92 / 12.04 vs 11.89 / 11.81 / 11.80 ms) and batch 32 (290.9 vs 290.9 ms): off
   static const int head = [] { const char* e = std::getenv("RC_GEMM_HEAD"); return e ? std::atoi(e) : 0; }();
   ep.head = head;
+  // k-block rotation: RC_GEMM_KROT 0 = off, 1 = launches with M <= 1024 (default), 2 = all
+  // measured neutral at cfg3 batch 1 (SwiGLU 5.53 vs 5.60 ms per step, transposed QKV 2.32 vs 2.31 ms
+  // in ncu; TTFT within noise) and slightly slower at batch 32 with every launch rotated (292.4 vs 288.5
+  // ms): off by default
+  static const int krot = [] { const char* e = std::getenv("RC_GEMM_KROT"); return e ? std::atoi(e) : 0; }();
+  ep.krot = krot == 2 || (krot == 1 && M <= 1024);
   static const int no_epi = [] { const char* e = std::getenv("RC_GEMM_NOEPI"); return e ? std::atoi(e) : 0; }();
   ep.no_epi = no_epi;
+  static const int hint = [] { const char* e = std::getenv("RC_GEMM_RASTER_HINT"); return e ? std::atoi(e) : 1; }();
+  ep.hint = hint;
   // small M (one request's selected rows): the transposed pair kernel keeps every 256-row MMA full
   if (a64 != nullptr && bn == 256 && gemm_use_transposed(M, N, epi, ep.head_dim, num_sms)) {
     switch (epi) {
