@@ -1221,10 +1221,12 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   int group_m = static_cast<int>(std::max<size_t>(
       2, std::min<size_t>(num_m, group_a_bytes / (static_cast<size_t>(2 * BM) * K * 2))));
   {  // raster by estimated DRAM traffic: m-groups re-read B once per group, n-groups re-read A
-    // default m-groups: the n-grouped raster with evict_last B / evict_first A measured slower at cfg3
-    // batch 32 (GEMMs 250.7 -> 261.5 ms per step) and raised the gate/up DRAM bytes 2.43 -> 5.74 GB per
-    // launch (A lines evicted before the group's other n-tiles read them)
-    static const int raster = [] { const char* e = std::getenv("RC_GEMM_RASTER"); return e ? std::atoi(e) : 0; }();
+    // RC_GEMM_RASTER: 0 = m-groups, 1 = n-groups, -1 (default) = n-groups for the residual projections
+    // when the estimate favours them. Measured at cfg3 batch 32 (ncu, plain loads): O-proj + down 3.05 ->
+    // 2.31 GB DRAM per launch and 110.2 -> 106.6 ms over 1.5 steps, while gate/up got worse (2.95 ->
+    // 4.64 GB, 159.9 -> 165.9 ms); with the L2 eviction hints (RC_GEMM_RASTER_HINT=1) every class got
+    // worse (A lines evicted before the group's other n-tiles read them)
+    static const int raster = [] { const char* e = std::getenv("RC_GEMM_RASTER"); return e ? std::atoi(e) : -1; }();
     static const size_t group_b_bytes = [] {
       const char* e = std::getenv("RC_GROUP_B_MB");
       return e ? static_cast<size_t>(std::atoi(e)) << 20 : GROUP_B_BYTES;
@@ -1234,7 +1236,7 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
     const int gn = static_cast<int>(std::max<size_t>(1, std::min<size_t>(num_n, group_b_bytes / static_cast<size_t>(band))));
     const double tm = band * (num_m + num_n * double((num_m + group_m - 1) / group_m));
     const double tn = band * (num_n + num_m * double((num_n + gn - 1) / gn));
-    if (raster == 1 || (raster == -1 && tn < 0.8 * tm)) group_m = -gn;
+    if (raster == 1 || (raster == -1 && EPI == EPI_ADD_F32 && tn < 0.8 * tm)) group_m = -gn;
   }
   return launch_pdl(k_gemm_pair<EPI>, dim3(grid), dim3(256), C::SMEM, s, *a, *b, c ? *c : *a, M, N, K, splits,
                     group_m, sk_tiles, ep);
@@ -1374,7 +1376,7 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   ep.krot = krot == 2 || (krot == 1 && M <= 1024);
   static const int no_epi = [] { const char* e = std::getenv("RC_GEMM_NOEPI"); return e ? std::atoi(e) : 0; }();
   ep.no_epi = no_epi;
-  static const int hint = [] { const char* e = std::getenv("RC_GEMM_RASTER_HINT"); return e ? std::atoi(e) : 1; }();
+  static const int hint = [] { const char* e = std::getenv("RC_GEMM_RASTER_HINT"); return e ? std::atoi(e) : 0; }();
   ep.hint = hint;
   // small M (one request's selected rows): the transposed pair kernel keeps every 256-row MMA full
   if (a64 != nullptr && bn == 256 && gemm_use_transposed(M, N, epi, ep.head_dim, num_sms)) {
