@@ -866,12 +866,45 @@ struct TCfg {
 
 struct TSched {
   int cid, ncl, nstripes, nfull, tail_n, splits, nk;
+  int pack = 0;  // 1: the 128-token tail tiles of two stripes share one slot (see at_packed)
   // the it-th unit of this pair: weight stripe s, first token t0, N' (ncols) and the K range. Tiles of
   // 256 tokens (the last one 128 when the remainder fits), round-robin over units in stripe-major
   // order: a stripe's token tiles are adjacent, so its 256 weight rows stream from HBM once. (Cutting
   // the stripes x tokens into equal contiguous ranges per pair balanced the waves but streamed every
   // stripe's weights 3x through L2: SwiGLU 3.9 -> 4.9 ms per cfg3 batch-1 step, not kept.)
+  // Packed schedule (no split-K, 128-token tail): the slots of stripes (2j, 2j + 1) are their 2 nfull
+  // full tiles and ONE slot holding both 128-token tails back to back, dealt round-robin; every slot is
+  // 256 token columns, so |Sel| = 625 costs 2.5 slots per stripe: SwiGLU at cfg3 batch 1 = 280 slots on
+  // 74 pairs = 4 rounds of 256 columns instead of up to 4.5 (the tails of 336 tiles dealt round-robin
+  // left every third pair with 1152 columns against a 969 average). A stripe's tiles stay in one round.
+  __device__ __forceinline__ bool at_packed(int it, int& s, int& t0, int& ncols, Unit& un) const {
+    const int per2 = 2 * nfull + 1;
+    const int nslots = (nstripes / 2) * per2 + ((nstripes & 1) ? nfull + 1 : 0);
+    int left = it, tt = 0;
+    for (int k = 0;; ++k) {
+      const int q = cid + k * ncl;
+      if (q >= nslots) return false;
+      const int j = q / per2, r = q % per2;
+      const bool last_odd = 2 * j + 1 >= nstripes;  // the odd stripe out: its tail has a slot alone
+      const int cnt = (r == 2 * nfull && !last_odd) ? 2 : 1;
+      if (left < cnt) {
+        if (last_odd) { s = 2 * j; tt = r; }
+        else if (r < 2 * nfull) { s = 2 * j + r / nfull; tt = r % nfull; }
+        else { s = 2 * j + left; tt = nfull; }
+        break;
+      }
+      left -= cnt;
+    }
+    const int ntt = nfull + 1;
+    t0 = tt * 256;
+    ncols = tt < nfull ? 256 : tail_n;
+    un.tile = s * ntt + tt;
+    un.kb0 = 0; un.kb1 = nk;
+    un.seg = 0; un.nseg = 1; un.slot = un.tile; un.seg_stride = 1;
+    return true;
+  }
   __device__ __forceinline__ bool at(int it, int& s, int& t0, int& ncols, Unit& un) const {
+    if (pack) return at_packed(it, s, t0, ncols, un);
     const int ntt = nfull + (tail_n > 0 ? 1 : 0);
     const int u = cid + it * ncl;
     if (u >= nstripes * ntt * splits) return false;
@@ -1043,8 +1076,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int nfull = M / 256, rem = M - nfull * 256;
-  const TSched sc{static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), N / 256, nfull,
-                  rem > 0 ? (rem <= 128 ? 128 : 256) : 0, splits, (K + BK - 1) / BK};
+  TSched sc{static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), N / 256, nfull,
+            rem > 0 ? (rem <= 128 ? 128 : 256) : 0, splits, (K + BK - 1) / BK};
+  sc.pack = ep.t_pack && splits == 1 && sc.tail_n == 128 && nfull >= 1;
   auto w_at = [&](int it, Unit& un, int& row) {
     int s, t0, ncols;
     if (!sc.at(it, s, t0, ncols, un)) return false;
@@ -1356,6 +1390,7 @@ bool gemm_use_transposed(int M, int N, int epi, int head_dim, int num_sms) {
   if (!(epi == EPI_ADD_F32 || epi == EPI_SWIGLU || (epi == EPI_QKV && head_dim == 128))) return false;
   if (mode == 1) return true;
   if (mode == 2) return M <= 1024;
+  if (mode == 3) return (epi == EPI_ADD_F32 || epi == EPI_SWIGLU) && M <= 1024;
   return epi == EPI_ADD_F32 && M <= 1024;
 }
 
@@ -1378,6 +1413,8 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
   ep.no_epi = no_epi;
   static const int hint = [] { const char* e = std::getenv("RC_GEMM_RASTER_HINT"); return e ? std::atoi(e) : 0; }();
   ep.hint = hint;
+  static const int t_pack = [] { const char* e = std::getenv("RC_GEMM_T_PACK"); return e ? std::atoi(e) : 1; }();
+  ep.t_pack = t_pack;
   // small M (one request's selected rows): the transposed pair kernel keeps every 256-row MMA full
   if (a64 != nullptr && bn == 256 && gemm_use_transposed(M, N, epi, ep.head_dim, num_sms)) {
     switch (epi) {

@@ -405,16 +405,18 @@ def _gemm_t_child(path):
     np.savez(path, logits=res["logits"], hidden=res["hidden"], sel_pos=res["sel_pos"], sel_off=np.asarray(res["sel_off"]))
 
 
-@pytest.mark.parametrize("mode", ["1", "0"])
+@pytest.mark.parametrize("mode", ["1", "0", "1-unpacked"])
 def test_transposed_gemm_modes_match_oracle(mode, tmp_path):
     """Every GEMM schedule choice end to end: RC_GEMM_T=1 puts the QKV (RoPE + K/V scatter), SwiGLU and
-    residual GEMMs of every layer on the transposed CTA-pair kernel, RC_GEMM_T=0 none of them (the knob
-    is read once per process: child process). Both must match O-SEL forced to their selection."""
+    residual GEMMs of every layer on the transposed CTA-pair kernel (two stripes' 128-token tails packed
+    in one slot where they apply; "-unpacked": RC_GEMM_T_PACK=0), RC_GEMM_T=0 none of them (the knobs
+    are read once per process: child process). All must match O-SEL forced to their selection."""
     import subprocess, sys, os
     path = str(tmp_path / "gemm_t.npz")
     code = ("import sys; sys.path.insert(0, %r); from tests.test_gpu_parity import _gemm_t_child; _gemm_t_child(%r)"
             % (os.getcwd(), path))
-    subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, RC_GEMM_T=mode), timeout=600)
+    env = dict(os.environ, RC_GEMM_T=mode.split("-")[0], RC_GEMM_T_PACK="0" if mode.endswith("unpacked") else "1")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
     z = np.load(path)
     wl = rcgen.MINI_L
     case = make_case(wl, n_req=2)
