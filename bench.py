@@ -98,7 +98,7 @@ class ClockSampler:
         self.f.flush()
         rows = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
         os.unlink(self.f.name)
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
@@ -108,11 +108,16 @@ class ClockSampler:
             mx = max(mx, m)
             if s > 300:  # under load
                 sm.append(s)
+                try:
+                    pw.append(float(r[3]))
+                except ValueError:
+                    pass
             for n, v in zip(names, r[5:9]):
                 if v.strip() == "Active":
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(rows)}
+                "samples": len(rows), "power_w_median": float(np.median(pw)) if pw else None,
+                "power_w_max": max(pw) if pw else None}
 
 
 # --------------------------------------------------------------------------- workload setup

@@ -38,7 +38,7 @@ constexpr int BM = 128, BK = 64;
 constexpr int WS_TILE = 128 * 256;  // floats of one workspace slot: [256 columns][128 lanes]
 // raster: group_m m-tiles share a sweep over n; the host sizes the group by the bytes of its A rows
 // (they must stay in L2 while the sweep streams B; B is re-read ceil(num_m / group_m) times).
-constexpr size_t GROUP_B_BYTES = size_t(56) << 20;  // n-grouped raster: B bands kept (evict_last) per group
+constexpr size_t GROUP_B_BYTES = size_t(56) << 20;  // n-grouped raster: weight bands kept in L2 per group
 constexpr size_t GROUP_A_BYTES = size_t(32) << 20;  // measured: gate/up at cfg3 b32 3.14 -> 3.07 ms, DRAM 3.1 -> 1.9 GB vs 16 MB
 
 template <int BN>
@@ -148,53 +148,6 @@ __device__ __forceinline__ bool unit_at(const Sched& sc, int it, Unit& un) {
   un.slot = static_cast<int>(t);
   un.seg_stride = (P + sc.sk_tiles - 1) / sc.sk_tiles + 1;  // >= nseg of every tail tile
   return true;
-}
-
-// ------------------------------------------------------------------ weight prefetch
-// The weight operand of a small-M GEMM streams from HBM once (batch 1: 436 MB per layer), so every
-// k-block's TMA load pays the HBM latency, which a 4-6 stage ring does not cover. The producer keeps
-// an L2 prefetch PF k-blocks ahead of its loads over its whole unit sequence (unit boundaries
-// included), and issues the first PF before griddepcontrol.wait: weights are never written by the
-// previous kernel, so they load while it drains. RC_GEMM_PF = distance in k-blocks (0 = off).
-int gemm_pf_distance() {
-  // default off: measured slower at both batch sizes (cfg3 b1 11.7 -> 12.7 ms, b32 287 -> 309 ms at
-  // distance 8; distances 4 and 16 alike): the prefetch issue itself costs the producer thread
-  static const int pf = [] { const char* e = std::getenv("RC_GEMM_PF"); return e ? std::atoi(e) : 0; }();
-  return pf;
-}
-template <class At>
-struct PfCursor {  // (unit, k-block) sequence of one producer; At(it, un, row) -> bool, row = weight row
-  At at;
-  int it = 0, kb = 0, kb1 = 0, row = 0;
-  bool ok = false;
-  __device__ __forceinline__ void start() {
-    Unit un;
-    ok = at(0, un, row);
-    kb = un.kb0; kb1 = un.kb1;
-  }
-  __device__ __forceinline__ void next() {
-    if (!ok) return;
-    if (++kb < kb1) return;
-    Unit un;
-    ok = at(++it, un, row);
-    kb = un.kb0; kb1 = un.kb1;
-  }
-};
-
-// k-block rotation (small M): CTAs that share an operand tile in the same wave all start its K loop
-// at k-block 0, so every k-block of the shared tile is requested by tens of SMs at once (at batch 1 the
-// 625 token rows are shared by every weight tile in flight). A unit whose weight tile index is `key`
-// walks its K range starting at (key % 16) / 16 of the way in, so the CTAs sharing a weight tile stay in
-// step (one HBM read) while those sharing the token tile are spread over 16 phases.
-__device__ __forceinline__ int kb_rot(const Unit& un, int key, int on) {
-  const int n = un.kb1 - un.kb0;
-  return on ? ((key & 15) * n) >> 4 : 0;
-}
-__device__ __forceinline__ int kb_at(const Unit& un, int i, int r) {
-  const int n = un.kb1 - un.kb0;
-  int j = i + r;
-  if (j >= n) j -= n;
-  return un.kb0 + j;
 }
 
 // group_m < 0: the transposed raster, -group_m n-tiles share a sweep over m (B stays in L2, A is
@@ -591,6 +544,8 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
+  griddep_launch();
 
   const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
@@ -598,62 +553,20 @@ __global__ void __launch_bounds__(256, 1)
   const int units = tiles * splits;
   Sched sc{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), units, splits, num_m, num_n, group_m, BM, 0};
   sc.nk = nk;
-  auto w_at = [&](int it, Unit& un, int& row) {
-    if (!unit_at(sc, it, un)) return false;
-    int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
-    row = nb * BN;
-    return true;
-  };
-  PfCursor<decltype(w_at)> pfc{w_at};
-  auto pf_issue = [&]() {  // the weight boxes of the cursor's k-block, then advance
-    if (!pfc.ok) return;
-#pragma unroll
-    for (int h = 0; h < BN / 128; ++h) tma_prefetch_l2_2d(&tmB, pfc.kb * BK, pfc.row + h * 128);
-    pfc.next();
-  };
-  if (warp == 0 && lane == 0 && ep.pf > 0) {  // weights only: safe before the PDL wait
-    pfc.start();
-    for (int i = 0; i < ep.pf; ++i) pf_issue();
-  }
-  // head loads: the weight boxes of the first k-blocks go into their (still free) stages before the
-  // PDL wait (weights are never produced by the previous kernel); their A boxes follow after it
-  int pre = 0;
-  if (warp == 0 && lane == 0 && ep.head > 0) {
-    Unit u0;
-    if (unit_at(sc, 0, u0)) {
-      int mb, nb; tile_coords(u0.tile, num_m, num_n, group_m, mb, nb);
-      const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
-      const int rot = kb_rot(u0, nb, ep.krot);
-      for (; pre < n; ++pre) {
-        mbar_expect_tx(&full[pre], C::A_BYTES + C::B_BYTES);
-#pragma unroll
-        for (int h = 0; h < BN / 128; ++h)
-          tma_load_2d(sB + pre * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[pre], kb_at(u0, pre, rot) * BK, nb * BN + h * 128);
-      }
-    }
-  }
-  griddep_wait();  // PDL: prologue above overlapped the previous kernel's tail
-  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
-      int stage = 0; uint32_t phase = 0, g = 0;
+      int stage = 0; uint32_t phase = 0;
       Unit un;
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
-        const int rot = kb_rot(un, nb, ep.krot);
-        for (int i = 0; i < un.kb1 - un.kb0; ++i, ++g) {
-          const int kb = kb_at(un, i, rot);
-          if (ep.pf > 0) pf_issue();
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          const bool head = g < static_cast<uint32_t>(pre);
-          if (!head) mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
+          mbar_expect_tx(&full[stage], C::A_BYTES + C::B_BYTES);
           tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, mb * BM);
-          if (!head) {
 #pragma unroll
-            for (int h = 0; h < BN / 128; ++h)  // B boxes are 128 rows (shared with the CTA-pair kernel)
-              tma_load_2d(sB + stage * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[stage], kb * BK, nb * BN + h * 128);
-          }
+          for (int h = 0; h < BN / 128; ++h)  // B boxes are 128 rows (shared with the CTA-pair kernel)
+            tma_load_2d(sB + stage * C::B_BYTES + h * 128 * BK * 2, &tmB, &full[stage], kb * BK, nb * BN + h * 128);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -668,14 +581,14 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int i = 0; i < un.kb1 - un.kb0; ++i) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (i != 0 || k != 0) ? 1u : 0u);
+            umma_bf16(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -742,6 +655,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();  // barrier inits and both TMEM allocations visible pair-wide
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
 
   const int num_m = (M + 2 * BM - 1) / (2 * BM), num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
   const int nk = (K + BK - 1) / BK;
@@ -752,65 +667,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   Sched sc{cid, ncl, units, splits, num_m, num_n, group_m, 2 * BM, static_cast<int>(rank) * BM};
   sc.nk = nk;
   sc.sk_tiles = sk_tiles;
-  auto w_at = [&](int it, Unit& un, int& row) {
-    if (!unit_at(sc, it, un)) return false;
-    int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
-    row = nb * BN + static_cast<int>(rank) * 128;  // this CTA's 128 weight rows
-    return true;
-  };
-  PfCursor<decltype(w_at)> pfc{w_at};
-  auto pf_issue = [&]() {
-    if (!pfc.ok) return;
-    tma_prefetch_l2_2d(&tmB, pfc.kb * BK, pfc.row);
-    pfc.next();
-  };
-  if (warp == 0 && lane == 0 && ep.pf > 0) {  // weights only: safe before the PDL wait
-    pfc.start();
-    for (int i = 0; i < ep.pf; ++i) pf_issue();
-  }
-  int pre = 0;  // head loads (see k_gemm): this CTA's weight half of the first k-blocks before the wait
-  if (warp == 0 && lane == 0 && ep.head > 0) {
-    Unit u0;
-    if (unit_at(sc, 0, u0)) {
-      int mb, nb; tile_coords(u0.tile, num_m, num_n, group_m, mb, nb);
-      const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
-      const int rot = kb_rot(u0, nb, ep.krot);
-      for (; pre < n; ++pre) {
-        if (leader) mbar_expect_tx(&full[pre], 2 * (C::A_BYTES + C::B_BYTES));
-        tma_load_2d_pair(sB + pre * C::B_BYTES, &tmB, leader_full + pre * 8, kb_at(u0, pre, rot) * BK,
-                         nb * BN + static_cast<int>(rank) * 128);
-      }
-    }
-  }
-  griddep_wait();
-  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
       Unit un;
-      // n-grouped raster: B resident across the group's waves, A streamed
-      const bool hint = group_m < 0 && ep.hint;
-      const uint64_t pol_a = l2_policy_evict_first(), pol_b = l2_policy_evict_last();
-      uint32_t g = 0;
       for (int it = 0; unit_at(sc, it, un); ++it) {
         int mb, nb; tile_coords(un.tile, num_m, num_n, group_m, mb, nb);
         const int arow = mb * 2 * BM + rank * BM, brow = nb * BN + rank * 128;
-        const int rot = kb_rot(un, nb, ep.krot);
-        for (int i = 0; i < un.kb1 - un.kb0; ++i, ++g) {
-          const int kb = kb_at(un, i, rot);
-          if (ep.pf > 0) pf_issue();
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
-          const bool head = g < static_cast<uint32_t>(pre);
-          if (leader && !head) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
-          if (hint) {
-            tma_load_2d_pair_hint(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow, pol_a);
-            if (!head) tma_load_2d_pair_hint(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow, pol_b);
-          } else {
-            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow);
-            if (!head) tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
-          }
+          if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + C::B_BYTES));
+          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, fb, kb * BK, arow);
+          tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, fb, kb * BK, brow);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -825,14 +695,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int i = 0; i < un.kb1 - un.kb0; ++i) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (i != 0 || k != 0) ? 1u : 0u);
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
           umma_commit_pair(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1074,64 +944,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
 
   const int nfull = M / 256, rem = M - nfull * 256;
   TSched sc{static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), N / 256, nfull,
             rem > 0 ? (rem <= 128 ? 128 : 256) : 0, splits, (K + BK - 1) / BK};
   sc.pack = ep.t_pack && splits == 1 && sc.tail_n == 128 && nfull >= 1;
-  auto w_at = [&](int it, Unit& un, int& row) {
-    int s, t0, ncols;
-    if (!sc.at(it, s, t0, ncols, un)) return false;
-    row = s * 256 + static_cast<int>(rank) * 128;  // this CTA's 128 weight rows
-    return true;
-  };
-  PfCursor<decltype(w_at)> pfc{w_at};
-  auto pf_issue = [&]() {
-    if (!pfc.ok) return;
-    tma_prefetch_l2_2d(&tmW, pfc.kb * BK, pfc.row);
-    pfc.next();
-  };
-  if (warp == 0 && lane == 0 && ep.pf > 0) {  // weights only: safe before the PDL wait
-    pfc.start();
-    for (int i = 0; i < ep.pf; ++i) pf_issue();
-  }
   const uint32_t leader_full = mapa_shared(full, 0);
   const uint32_t leader_tempty = mapa_shared(tempty, 0);
-  int pre = 0;  // head loads (see k_gemm): this CTA's weight rows of the first k-blocks before the wait
-  if (warp == 0 && lane == 0 && ep.head > 0) {
-    int s0, t00, nc0;
-    Unit u0;
-    if (sc.at(0, s0, t00, nc0, u0)) {
-      const int n = min(min(ep.head, static_cast<int>(C::STAGES)), u0.kb1 - u0.kb0);
-      const int rot = kb_rot(u0, s0, ep.krot);
-      for (; pre < n; ++pre) {
-        if (leader) mbar_expect_tx(&full[pre], 2 * (C::A_BYTES + static_cast<uint32_t>(nc0 / 2) * BK * 2));
-        tma_load_2d_pair(sA + pre * C::A_BYTES, &tmW, leader_full + pre * 8, kb_at(u0, pre, rot) * BK,
-                         s0 * 256 + static_cast<int>(rank) * 128);
-      }
-    }
-  }
-  griddep_wait();
-  griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs)
-      int stage = 0; uint32_t phase = 0, g = 0;
+      int stage = 0; uint32_t phase = 0;
       int s, t0, ncols;
       Unit un;
       for (int it = 0; sc.at(it, s, t0, ncols, un); ++it) {
         const int wrow = s * 256 + rank * 128;
         const int half = ncols / 2;
         const int trow = t0 + rank * half;
-        const int rot = kb_rot(un, s, ep.krot);
-        for (int i = 0; i < un.kb1 - un.kb0; ++i, ++g) {
-          const int kb = kb_at(un, i, rot);
-          if (ep.pf > 0) pf_issue();
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
-          const bool head = g < static_cast<uint32_t>(pre);
-          if (leader && !head) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2));
-          if (!head) tma_load_2d_pair(sA + stage * C::A_BYTES, &tmW, fb, kb * BK, wrow);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (C::A_BYTES + static_cast<uint32_t>(half) * BK * 2));
+          tma_load_2d_pair(sA + stage * C::A_BYTES, &tmW, fb, kb * BK, wrow);
           // one box per CTA: 128 token rows (full tile) or 64 (tail); the TMA issue count matters (four
           // 32-row boxes per full tile measured 12 % slower than two 64-row boxes at cfg3 batch 1)
           tma_load_2d_pair(sB + stage * C::B_BYTES, half == 128 ? &tmX128 : &tmX64, fb, kb * BK, trow);
@@ -1150,14 +986,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         tc_fence_after();
         const uint32_t idesc = idesc_bf16_f32(256, ncols);
         const uint32_t d_tmem = tmem_base + acc * 256;
-        for (int i = 0; i < un.kb1 - un.kb0; ++i) {
+        for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + stage * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (i != 0 || k != 0) ? 1u : 0u);
+            umma_bf16_pair(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (kb != un.kb0 || k != 0) ? 1u : 0u);
           umma_commit_pair(&empty[stage]);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -1256,10 +1092,10 @@ cudaError_t launch_pair(const CUtensorMap* a, const CUtensorMap* b, const CUtens
       2, std::min<size_t>(num_m, group_a_bytes / (static_cast<size_t>(2 * BM) * K * 2))));
   {  // raster by estimated DRAM traffic: m-groups re-read B once per group, n-groups re-read A
     // RC_GEMM_RASTER: 0 = m-groups, 1 = n-groups, -1 (default) = n-groups for the residual projections
-    // when the estimate favours them. Measured at cfg3 batch 32 (ncu, plain loads): O-proj + down 3.05 ->
-    // 2.31 GB DRAM per launch and 110.2 -> 106.6 ms over 1.5 steps, while gate/up got worse (2.95 ->
-    // 4.64 GB, 159.9 -> 165.9 ms); with the L2 eviction hints (RC_GEMM_RASTER_HINT=1) every class got
-    // worse (A lines evicted before the group's other n-tiles read them)
+    // when the estimate favours them. Measured at cfg3 batch 32 (ncu): O-proj + down 3.05 -> 2.31 GB DRAM
+    // per launch and 110.2 -> 106.6 ms over 1.5 steps, while gate/up got worse (2.95 -> 4.64 GB, 159.9 ->
+    // 165.9 ms); L2 eviction-priority hints on top (evict_last weights, evict_first activations; removed)
+    // made every class worse: the activation lines left L2 before the group's other n-tiles read them
     static const int raster = [] { const char* e = std::getenv("RC_GEMM_RASTER"); return e ? std::atoi(e) : -1; }();
     static const size_t group_b_bytes = [] {
       const char* e = std::getenv("RC_GROUP_B_MB");
@@ -1398,23 +1234,10 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
                         int epi, const EpiArgs& ep_in, int num_sms, cudaStream_t s, const CUtensorMap* a64) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   EpiArgs ep = ep_in;
-  ep.pf = gemm_pf_distance();
-  // head loads (weights of the first k-blocks before the PDL wait): parity-green, within noise at cfg3
-  // batch 1 (11.89 / 11.92 / 12.04 vs 11.89 / 11.81 / 11.80 ms) and batch 32 (290.9 vs 290.9 ms): off
-  static const int head = [] { const char* e = std::getenv("RC_GEMM_HEAD"); return e ? std::atoi(e) : 0; }();
-  ep.head = head;
-  // k-block rotation: RC_GEMM_KROT 0 = off, 1 = launches with M <= 1024 (default), 2 = all
-  // measured neutral at cfg3 batch 1 (SwiGLU 5.53 vs 5.60 ms per step, transposed QKV 2.32 vs 2.31 ms
-  // in ncu; TTFT within noise) and slightly slower at batch 32 with every launch rotated (292.4 vs 288.5
-  // ms): off by default
-  static const int krot = [] { const char* e = std::getenv("RC_GEMM_KROT"); return e ? std::atoi(e) : 0; }();
-  ep.krot = krot == 2 || (krot == 1 && M <= 1024);
-  static const int no_epi = [] { const char* e = std::getenv("RC_GEMM_NOEPI"); return e ? std::atoi(e) : 0; }();
-  ep.no_epi = no_epi;
-  static const int hint = [] { const char* e = std::getenv("RC_GEMM_RASTER_HINT"); return e ? std::atoi(e) : 0; }();
-  ep.hint = hint;
   static const int t_pack = [] { const char* e = std::getenv("RC_GEMM_T_PACK"); return e ? std::atoi(e) : 1; }();
+  static const int no_epi = [] { const char* e = std::getenv("RC_GEMM_NOEPI"); return e ? std::atoi(e) : 0; }();
   ep.t_pack = t_pack;
+  ep.no_epi = no_epi;
   // small M (one request's selected rows): the transposed pair kernel keeps every 256-row MMA full
   if (a64 != nullptr && bn == 256 && gemm_use_transposed(M, N, epi, ep.head_dim, num_sms)) {
     switch (epi) {

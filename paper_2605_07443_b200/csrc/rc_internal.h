@@ -94,10 +94,6 @@ struct EpiArgs {
   int* ws_cnt = nullptr;    // 2 * gemm_ws_slots()
   int32_t ws_slots = 0;
   int32_t det = 1;          // 0: partial tiles reduce-add straight into x in arrival order
-  int32_t pf = 0;           // weight L2-prefetch distance in k-blocks (set by gemm_launch)
-  int32_t head = 0;         // k-blocks whose weight boxes load before the PDL wait (set by gemm_launch)
-  int32_t krot = 0;         // rotate each unit's k-block order by its weight tile (set by gemm_launch)
-  int32_t hint = 0;         // n-grouped raster: L2 eviction-priority hints on its loads (RC_GEMM_RASTER_HINT)
   int32_t t_pack = 0;       // transposed kernel: two stripes' 128-token tails share a slot (RC_GEMM_T_PACK)
   int32_t no_epi = 0;       // diagnostics: transposed kernel skips its epilogue (RC_GEMM_NOEPI)
 };
