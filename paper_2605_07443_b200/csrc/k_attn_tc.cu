@@ -188,17 +188,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // padding rows see no key: base 0 keeps them off the max-first path (their P is 0, l stays 0)
     float m_run = valid ? -INFINITY : 0.f, l_run = 0.f;
     uint32_t sr[SCOLS];
+    // S of the next step already requested (its TMEM load issued before this step's P store was
+    // fenced and signalled, when the probe found S_{j+1} complete): the load latency overlaps that hand-off
+    bool have_next = false;
     for (int j = 0; j < nkv; ++j) {
       const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      tc_fence_after();
       if (a.debug_mode & 1) {  // diagnostics: no softmax work
+        mbar_wait(&s_full[b], (j >> 1) & 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[b * 2 + h]);
         continue;
       }
-      tmem_ld32(tmem + lane_base + b * 128 + col0, sr);
-      tmem_ld32(tmem + lane_base + b * 128 + col0 + 32, sr + 32);
+      if (!have_next) {
+        mbar_wait(&s_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        tmem_ld32(tmem + lane_base + b * 128 + col0, sr);
+        tmem_ld32(tmem + lane_base + b * 128 + col0 + 32, sr + 32);
+      }
+      have_next = false;
       tmem_wait_ld();
       const int key0 = (j0 + j) * BKV + col0;
       const bool full = key0 + SCOLS - 1 <= p_first;  // every row sees every key of the half: no mask
@@ -212,6 +219,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
           l_run += ls;
           tmem_st32(tmem + lane_base + b * 128 + col0, pk);
+          if (a.s_prefetch && j + 1 < nkv &&
+              __any_sync(0xffffffffu, mbar_test(&s_full[b ^ 1], ((j + 1) >> 1) & 1))) {
+            mbar_wait(&s_full[b ^ 1], ((j + 1) >> 1) & 1);  // complete for every lane: returns at once
+            tc_fence_after();
+            tmem_ld32(tmem + lane_base + (b ^ 1) * 128 + col0, sr);
+            tmem_ld32(tmem + lane_base + (b ^ 1) * 128 + col0 + 32, sr + 32);
+            have_next = true;
+          }
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();

@@ -1110,6 +1110,8 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
   if (zc_layer && c->attn_tc) at.vsrc = layer_vsrc(c, l);  // NEXT-4: item / prefix V read in place
   static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
   at.debug_mode = attn_debug;
+  static const int s_prefetch = std::getenv("RC_ATTN_SPREFETCH") ? std::atoi(std::getenv("RC_ATTN_SPREFETCH")) : 1;
+  at.s_prefetch = s_prefetch;
   at.n_splits = n_splits;
   at.split_min = split_min;
   if (paired == 2) at.chunk_per_cta = attn_chunk_per_cta();
