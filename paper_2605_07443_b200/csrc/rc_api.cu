@@ -1110,7 +1110,9 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
   if (zc_layer && c->attn_tc) at.vsrc = layer_vsrc(c, l);  // NEXT-4: item / prefix V read in place
   static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
   at.debug_mode = attn_debug;
-  static const int s_prefetch = std::getenv("RC_ATTN_SPREFETCH") ? std::atoi(std::getenv("RC_ATTN_SPREFETCH")) : 1;
+  // S_{j+1} TMEM load before the P_j hand-off: parity-green, measured slower at cfg3 batch 1 (attention
+  // 1.59-1.60 -> 1.65 ms per step, 42.5 -> 44.0 us per selective-layer launch in ncu): off by default
+  static const int s_prefetch = std::getenv("RC_ATTN_SPREFETCH") ? std::atoi(std::getenv("RC_ATTN_SPREFETCH")) : 0;
   at.s_prefetch = s_prefetch;
   at.n_splits = n_splits;
   at.split_min = split_min;
