@@ -55,7 +55,8 @@ def test_gemm_matches_exact_matmul(M, N, K, bn):
 
 @pytest.mark.parametrize("M,N,K,trans", [(625, 4096, 4096, True), (625, 4096, 14336, True), (113, 1024, 640, True),
                                          (395, 512, 2048, True), (1000, 768, 4096, True), (3889, 4096, 4096, False),
-                                         (625, 4096, 14336, False), (200, 512, 4096, False), (4096, 1024, 1024, False)])
+                                         (625, 4096, 14336, False), (200, 512, 4096, False), (4096, 1024, 1024, False),
+                                         (5000, 4096, 14336, False)])  # the last: n-grouped raster (default for it)
 def test_residual_gemm_exact_and_reproducible(M, N, K, trans):
     """x += A B^T through every residual-GEMM schedule (transposed pair tiles with a ragged token tail,
     split-K, the stream-K tail, whole tiles): equal to the exact product added to x, and bitwise the
