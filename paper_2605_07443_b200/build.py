@@ -16,6 +16,8 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-fvisibility=hidden", "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr", "-Xptxas", "-v",
          "-I", os.path.join(HERE, "..", "include")]
+# diagnostics builds only (e.g. RC_BUILD_DEFS=-DRC_ATTN_PROF for the attention phase timing); rebuild with --force
+FLAGS += os.environ.get("RC_BUILD_DEFS", "").split()
 SOURCES = ["rc_api.cu", "rc_place.cu", "k_gemm.cu", "k_gather.cu", "k_attn.cu", "k_attn_tc.cu", "k_attn_pair.cu", "k_attn_mass.cu", "k_semlib.cu", "k_small.cu"]
 
 

@@ -48,6 +48,17 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 constexpr unsigned POLY_CHUNKS = 0x44;
 constexpr float SPEC_SUM_MAX = 18446744073709551616.0f;  // 2^64: bound of the speculative exps' row sum
 constexpr int N_ITEM_CONSUMERS = 2 + 8;    // MMA thread, V producer, 8 softmax warps
+// Phase timing (diagnostics build only: -DRC_ATTN_PROF, env RC_ATTN_PROF=1 at run time): clock64 sums
+// per role and phase, added to a.prof at the end -- [0] softmax waits for S, [1] TMEM load of S,
+// [2] exp/pack, [3] P store + fence + arrival, [4] item epilogue, [5] MMA waits for P, [6] MMA waits for
+// K/V, [7] MMA thread total, [8] softmax total
+#ifdef RC_ATTN_PROF
+#define PROF_NOW(v) const long long v = clock64()
+#define PROF_ADD(i, d) (prof_acc[i] += static_cast<unsigned long long>(d))
+#else
+#define PROF_NOW(v)
+#define PROF_ADD(i, d)
+#endif
 
 // Persistent: grid <= #SMs, each CTA takes work items (tile pair, kv head) from a global counter,
 // longest pairs first, so the next item's Q/K/V loads and first S MMAs overlap the previous item's
@@ -283,6 +294,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
+#ifdef RC_ATTN_PROF
+      unsigned long long prof_acc[9] = {};
+      const long long t_start = clock64();
+#endif
       constexpr uint32_t idS = idesc_bf16_f32(128, 128);
       constexpr uint32_t idPV = idesc_bf16_f32_bmn(128, 128);
       const bool no_mma = (a.debug_mode & 2) != 0;  // diagnostics: barriers only
@@ -314,7 +329,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         umma_commit(&k_empty[kc % KST]);
         for (int j = 0; j < it.nkv; ++j) {
           const int v = (vc + j) % VST;
+          PROF_NOW(tv0);
           mbar_wait(&v_full[v], ((vc + j) / VST) & 1);
+          PROF_NOW(tv1);
+          PROF_ADD(6, tv1 - tv0);
           if (a.vsrc.vmap) fence_proxy_async();  // zero-copy V: cp.async (generic proxy) writes -> MMA reads
           tc_fence_after();
           bool k_ready = false;
@@ -322,7 +340,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int t = 0; t < 2; ++t) {
             if (j >= it.nk[t]) continue;
             if (j == 0 && n_done[t] > 0) mbar_wait(&o_free[t], (n_done[t] - 1) & 1);  // O_t read out
+            PROF_NOW(tp0);
             mbar_wait(&p_full[t], pc[t] & 1);
+            PROF_NOW(tp1);
+            PROF_ADD(5, tp1 - tp0);
             ++pc[t];
             tc_fence_after();
 #pragma unroll
@@ -344,12 +365,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         umma_commit(q_empty);
         kc += it.nkv;
+#ifdef RC_ATTN_PROF
+        prof_acc[7] = clock64() - t_start;
+#endif
         vc += it.nkv;
 #pragma unroll
         for (int t = 0; t < 2; ++t) n_done[t] += it.nk[t] > 0 ? 1 : 0;
       }
+#ifdef RC_ATTN_PROF
+      if (a.prof) for (int i = 5; i < 8; ++i) atomicAdd(a.prof + i, prof_acc[i]);
+#endif
     }
   } else if (warp >= 4) {  // ---- softmax: tile t, thread <-> row
+#ifdef RC_ATTN_PROF
+    unsigned long long prof_acc[9] = {};
+    const long long t_start = clock64();
+#endif
     const int t = (warp - 4) >> 2;
     const int q = warp & 3;  // TMEM lane quarter of this warp
     const int r = q * 32 + lane;
@@ -371,8 +402,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // padding rows see no key: base 0 keeps them off the max-first path (their P is 0, l stays 0)
       float m_run = valid ? -INFINITY : 0.f, l_run = 0.f;
       for (int j = 0; j < n_t; ++j, ++sc) {
+        PROF_NOW(tw0);
         mbar_wait(&s_full[t], sc & 1);
         tc_fence_after();
+        PROF_NOW(tw1);
+        PROF_ADD(0, tw1 - tw0);
         if (a.debug_mode & 1) {  // diagnostics: no softmax work
           __syncwarp();
           if (lane == 0) mbar_arrive(&p_full[t]);
@@ -381,9 +415,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
           uint32_t sr[64];
+          PROF_NOW(th0);
           tmem_ld32(s_col + hh * 64, sr);
           tmem_ld32(s_col + hh * 64 + 32, sr + 32);
           tmem_wait_ld();
+          PROF_NOW(th1);
+          PROF_ADD(1, th1 - th0);
           const int key0 = (it.c0 + j) * BKV + hh * 64;
           const bool full = key0 + 63 <= p_first;  // every row sees every key of the half: no causal mask
           uint32_t pk[32];
@@ -396,6 +433,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (!__any_sync(0xffffffffu, !(ls <= SPEC_SUM_MAX))) {
               l_run += ls;
               tmem_st32(s_col + hh * 32, pk);
+              PROF_NOW(th2);
+              PROF_ADD(2, th2 - th1);
               continue;
             }
           }
@@ -439,11 +478,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         : sm_exp_pack64<true, POLY_CHUNKS>(sr, pk, key0, p, a.scale_log2, base);
           tmem_st32(s_col + hh * 32, pk);  // P of keys [64 hh, 64 hh + 64) -> columns [32 hh, 32 hh + 32)
         }
+        PROF_NOW(ts0);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t]);
+        PROF_NOW(ts1);
+        PROF_ADD(3, ts1 - ts0);
       }
+      PROF_NOW(te0);
       mbar_wait(&o_done[t], od & 1);
       ++od;
       tc_fence_after();
@@ -529,7 +572,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
+      PROF_NOW(te1);
+      PROF_ADD(4, te1 - te0);
     }
+#ifdef RC_ATTN_PROF
+    prof_acc[8] = clock64() - t_start;
+    if (lane == 0 && a.prof)
+      for (int i = 0; i < 9; ++i) if (i != 5 && i != 6 && i != 7) atomicAdd(a.prof + i, prof_acc[i]);
+#endif
   }
   tc_fence_before();
   __syncthreads();

@@ -243,6 +243,7 @@ struct rc_ctx {
   float* part_ml = nullptr;
   int32_t* part_flag = nullptr;  // KV split: arrival counter per (logical tile, KV head)
   int32_t* attn_ctr = nullptr;   // paired attention work counter
+  unsigned long long* attn_prof = nullptr;  // diagnostics: paired-attention phase cycle sums (RC_ATTN_PROF)
   size_t part_rows = 0;
   int32_t* sel_pos = nullptr;
   int32_t* sel_dst = nullptr;
@@ -644,7 +645,21 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   return RC_OK;
 }
 
-void rc_destroy(rc_ctx* ctx) { delete ctx; }
+void rc_destroy(rc_ctx* ctx) {
+  if (ctx && ctx->attn_prof) {  // diagnostics: paired-attention phase timing (RC_ATTN_PROF=1)
+    unsigned long long h[16] = {};
+    cudaSetDevice(ctx->device);
+    if (cudaMemcpy(h, ctx->attn_prof, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      const char* nm[9] = {"softmax: wait S", "softmax: TMEM load S", "softmax: exp/pack", "softmax: P store+fence+arrive",
+                           "softmax: item epilogue", "mma: wait P", "mma: wait K/V", "mma: total", "softmax: total"};
+      for (int i = 0; i < 9; ++i)
+        fprintf(stderr, "RC_ATTN_PROF %-30s %14llu cycles  %6.3f of its role total\n", nm[i], h[i],
+                static_cast<double>(h[i]) / static_cast<double>(i >= 5 && i <= 7 ? (h[7] ? h[7] : 1) : (h[8] ? h[8] : 1)));
+    }
+    cudaFree(ctx->attn_prof);
+  }
+  delete ctx;
+}
 
 rc_status rc_decompose_prompt(const rc_prompt* pr, int32_t cap, int32_t* n_out, int32_t* token_ids, uint8_t* cls,
                               int64_t* src_id, int32_t* src_off, int32_t* seg_start) {
@@ -1110,6 +1125,13 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
   if (zc_layer && c->attn_tc) at.vsrc = layer_vsrc(c, l);  // NEXT-4: item / prefix V read in place
   static const int attn_debug = std::getenv("RC_ATTN_DEBUG") ? std::atoi(std::getenv("RC_ATTN_DEBUG")) : 0;
   at.debug_mode = attn_debug;
+  static const bool attn_prof = std::getenv("RC_ATTN_PROF") && std::atoi(std::getenv("RC_ATTN_PROF")) == 1;
+  if (attn_prof && !c->attn_prof) {
+    cudaError_t e = cudaSuccess;
+    c->attn_prof = dev_alloc<unsigned long long>(16, &e);
+    if (e == cudaSuccess) cudaMemset(c->attn_prof, 0, 16 * sizeof(unsigned long long));
+  }
+  at.prof = c->attn_prof;
   // S_{j+1} TMEM load before the P_j hand-off: parity-green, measured slower at cfg3 batch 1 (attention
   // 1.59-1.60 -> 1.65 ms per step, 42.5 -> 44.0 us per selective-layer launch in ncu): off by default
   static const int s_prefetch = std::getenv("RC_ATTN_SPREFETCH") ? std::atoi(std::getenv("RC_ATTN_SPREFETCH")) : 0;

@@ -193,6 +193,7 @@ struct AttnArgs {
   // (all pair-steps) / (chunk_per_cta * grid) KV tiles; partials per chunk in part_o / part_ml at slot
   // ((tile * Hk + kvh) * ATTN_MAX_CHUNKS + chunk), merged by the last-arriving chunk (split_flag)
   float chunk_per_cta = 0.f;
+  unsigned long long* prof = nullptr;  // paired kernel phase timing (-DRC_ATTN_PROF builds, RC_ATTN_PROF=1)
   int32_t s_prefetch = 0;  // single-tile kernel: load S_{j+1} from TMEM before signalling P_j (RC_ATTN_SPREFETCH)
   VSrc vsrc;                      // zero-copy V: V rows through vmap (cp.async loads) instead of TMA boxes
 };
