@@ -1218,8 +1218,12 @@ int gemm_ws_slots() { return 512; }
 int gemm_t_box_rows() { return 64; }
 size_t gemm_ws_floats() { return static_cast<size_t>(gemm_ws_slots()) * WS_TILE; }
 
-// RC_GEMM_T: 0 never, 1 every eligible GEMM at any M, 2 every eligible GEMM at M <= 1024; default:
-// the residual GEMMs at M <= 1024 (where it measured faster than split-K CTA pairs at cfg3 batch 1)
+// RC_GEMM_T: 0 never, 1 every eligible GEMM at any M, 2 every eligible GEMM at M <= 1024, 3 residual and
+// SwiGLU at M <= 1024, 4 residual only; default: the residual GEMMs at M <= 1024 (where it measured faster than split-K
+// CTA pairs at cfg3 batch 1) and the SwiGLU at M <= 512. SwiGLU, cfg3 batch-1 GEMM ms per step, default
+// single-CTA vs transposed, two passes on one box (profiles/r02_ab_dispatch.sh): r = 5 % (M ~ 205)
+// 6.40 / 6.27 vs 6.13 / 6.14, r = 10 % 8.38 / 8.41 vs 8.20 / 8.12, r = 15 % (M 625) 9.37 / 9.41 vs
+// 9.50 / 9.48, r = 20 % 13.80 / 13.79 vs 13.92 / 13.88
 bool gemm_use_transposed(int M, int N, int epi, int head_dim, int num_sms) {
   static const int mode = [] { const char* e = std::getenv("RC_GEMM_T"); return e ? std::atoi(e) : -1; }();
   if (mode == 0 || M <= 0 || N % 256 || num_sms < 2) return false;
@@ -1227,7 +1231,8 @@ bool gemm_use_transposed(int M, int N, int epi, int head_dim, int num_sms) {
   if (mode == 1) return true;
   if (mode == 2) return M <= 1024;
   if (mode == 3) return (epi == EPI_ADD_F32 || epi == EPI_SWIGLU) && M <= 1024;
-  return epi == EPI_ADD_F32 && M <= 1024;
+  if (mode == 4) return epi == EPI_ADD_F32 && M <= 1024;  // the round-2 default before the SwiGLU rule (A/B)
+  return (epi == EPI_ADD_F32 && M <= 1024) || (epi == EPI_SWIGLU && M <= 512);
 }
 
 cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtensorMap* c, int M, int N, int K, int bn,
