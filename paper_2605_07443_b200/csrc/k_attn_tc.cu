@@ -371,9 +371,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   }
+  // early O-projection (a.ready): this CTA's output rows are written; count it on every 256-row token
+  // tile its rows touch, so the next kernel (the transposed O-proj, launched early by PDL) can start the
+  // token tiles whose attention is complete while the longest tiles still run
+  if (a.ready) __threadfence();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (a.ready && threadIdx.x == 0 && n_rows > 0 && nsp == 1)
+    for (int tt = row_start / 256; tt <= (row_start + n_rows - 1) / 256; ++tt) atomicAdd(a.ready + tt, 1);
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 

@@ -734,9 +734,27 @@ struct TCfg {
   static constexpr uint32_t TMEM_COLS = 512;
 };
 
+// early O-projection: wait until `target` attention CTAs have signalled the token tile (acquire), then
+// order this thread's later TMA (async-proxy) reads after the generic-proxy writes it synchronised with.
+// Bounded: a signal that never comes traps (a launch error) instead of hanging the GPU.
+__device__ __forceinline__ void wait_ready(const int32_t* ctr, int target) {
+  const long long t_start = clock64();
+  while (true) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    __nanosleep(128);
+    if (clock64() - t_start > (1ll << 33)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 struct TSched {
   int cid, ncl, nstripes, nfull, tail_n, splits, nk;
   int pack = 0;  // 1: the 128-token tail tiles of two stripes share one slot (see at_packed)
+  int ttmajor = 0;  // 1 (early O-projection): token tile major, so every pair's first units are the
+                    // token tiles whose attention finishes first (short causal ranges) and the last
+                    // token tile's units come last
   // the it-th unit of this pair: weight stripe s, first token t0, N' (ncols) and the K range. Tiles of
   // 256 tokens (the last one 128 when the remainder fits), round-robin over units in stripe-major
   // order: a stripe's token tiles are adjacent, so its 256 weight rows stream from HBM once. (Cutting
@@ -779,8 +797,8 @@ struct TSched {
     const int u = cid + it * ncl;
     if (u >= nstripes * ntt * splits) return false;
     const int tile = u / splits, sp = u % splits;
-    s = tile / ntt;
-    const int tt = tile % ntt;
+    s = ttmajor ? tile % nstripes : tile / ntt;
+    const int tt = ttmajor ? tile / nstripes : tile % ntt;
     t0 = tt * 256;
     ncols = tt < nfull ? 256 : tail_n;
     un.tile = tile;
@@ -944,13 +962,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  griddep_wait();
+  // early O-projection: the only input the previous kernel (attention) produces is the token operand,
+  // gated per token tile by ep.ready below; everything older completed before any attention CTA
+  // passed its own griddepcontrol.wait
+  if (ep.ready == nullptr) griddep_wait();
   griddep_launch();
 
   const int nfull = M / 256, rem = M - nfull * 256;
   TSched sc{static_cast<int>(blockIdx.x >> 1), static_cast<int>(gridDim.x >> 1), N / 256, nfull,
             rem > 0 ? (rem <= 128 ? 128 : 256) : 0, splits, (K + BK - 1) / BK};
-  sc.pack = ep.t_pack && splits == 1 && sc.tail_n == 128 && nfull >= 1;
+  sc.pack = ep.t_pack && splits == 1 && sc.tail_n == 128 && nfull >= 1 && ep.ready == nullptr;
+  sc.ttmajor = ep.ready != nullptr;
   const uint32_t leader_full = mapa_shared(full, 0);
   const uint32_t leader_tempty = mapa_shared(tempty, 0);
 
@@ -963,6 +985,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const int wrow = s * 256 + rank * 128;
         const int half = ncols / 2;
         const int trow = t0 + rank * half;
+        if (ep.ready) wait_ready(ep.ready + t0 / 256, ep.ready_tgt[t0 / 256]);
         for (int kb = un.kb0; kb < un.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = leader_full + stage * 8;
@@ -1036,6 +1059,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  if (ep.ready && threadIdx.x == 0) {  // the last CTA to finish zeroes the token-tile counters
+    __threadfence();
+    if (atomicAdd(ep.ready + 4, 1) == static_cast<int>(gridDim.x) - 1) {
+#pragma unroll
+      for (int i = 0; i < 5; ++i) atomicExch(ep.ready + i, 0);
+      __threadfence();
+    }
+  }
 }
 
 // split-K: minimise waves * (k-blocks per unit + ~6 k-blocks of fixed per-unit cost) + the ordered
@@ -1252,6 +1283,7 @@ cudaError_t gemm_launch(const CUtensorMap* a, const CUtensorMap* b, const CUtens
       default: break;
     }
   }
+  if (ep.ready != nullptr) return cudaErrorInvalidValue;  // early O-projection needs the transposed kernel
   // CTA pairs for 256-wide GEMMs with M >= 1024: at cfg3 batch 32 they lift the GEMMs from 0.92 to
   // 0.99 of the measured sustained peak. RC_GEMM_PAIR=0/1 forces.
   static const int pair_mode = [] { const char* e = std::getenv("RC_GEMM_PAIR"); return e ? std::atoi(e) : -1; }();

@@ -243,6 +243,11 @@ struct rc_ctx {
   float* part_ml = nullptr;
   int32_t* part_flag = nullptr;  // KV split: arrival counter per (logical tile, KV head)
   int32_t* attn_ctr = nullptr;   // paired attention work counter
+  // early O-projection at small M (one request's Sel): per 256-row token tile, the attention CTAs done
+  // with it ([0..3]) and the O-proj CTAs finished ([4]); zeroed by the O-proj's last CTA
+  int32_t* oproj_ready = nullptr;
+  bool early_on = false;         // set around the selective layers when their tile list allows it
+  int32_t early_cnt[4] = {};     // attention CTAs per token tile of that list
   unsigned long long* attn_prof = nullptr;  // diagnostics: paired-attention phase cycle sums (RC_ATTN_PROF)
   size_t part_rows = 0;
   int32_t* sel_pos = nullptr;
@@ -294,7 +299,7 @@ struct rc_ctx {
     for (auto& p : pend) cudaFreeHost(p.host);
     void* bufs[] = {wqkv, bqkv, wgu, item_pool, hist_q, hist_s, prefix_pool, arena, rope_cos, rope_sin, x, xs,
                     a, q, o, h, dev, logits, sel_pos, sel_dst, sel_urow, part_o, part_ml, part_flag, mass_k, mass_v,
-                    mass_lse, mass_a, attn_ctr, gemm_ws, gemm_cnt, vmap, proto_tab, dev_err, grad_buf};
+                    mass_lse, mass_a, attn_ctr, oproj_ready, gemm_ws, gemm_cnt, vmap, proto_tab, dev_err, grad_buf};
     for (void* p : bufs)
       if (p) cudaFree(p);
     if (host_pool) cudaFreeHost(host_pool);
@@ -603,6 +608,8 @@ rc_status rc_create(const rc_model_desc* md, const rc_weights* w, const rc_pool_
   // tensor maps: A operands (rows = Mx; tiles never read beyond the call's M-tile), B = weights
   c->gemm_ws = dev_alloc<float>(gemm_ws_floats(), &e); if (e) return fail(RC_E_NOMEM, "gemm workspace");
   c->gemm_cnt = dev_alloc<int>(2 * gemm_ws_slots(), &e); if (e) return fail(RC_E_NOMEM, "gemm workspace");
+  c->oproj_ready = dev_alloc<int32_t>(8, &e); if (e) return fail(RC_E_NOMEM, "early O-projection counters");
+  RC_CUDA(cudaMemset(c->oproj_ready, 0, 8 * sizeof(int32_t)));
   RC_CUDA(cudaMemset(c->gemm_cnt, 0, 2 * gemm_ws_slots() * sizeof(int)));
   bool ok = make_tmap_bf16_2d(&c->mA_a, c->a, Mx, d, d, 128) &&
             make_tmap_bf16_2d(&c->mA_o, c->o, Mx, H * dh, H * dh, 128) &&
@@ -1165,6 +1172,16 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
     if (e != cudaSuccess) return fail(RC_E_NOMEM, "attention work counter");
   }
   at.work_ctr = c->attn_ctr;
+  // early O-projection (RC_OPROJ_EARLY=1, opt-in): with the single-tile attention unsplit and the O-proj
+  // on the transposed kernel, the O-proj's units wait per 256-row token tile for the attention CTAs
+  // that write it instead of for the whole attention grid (its longest causal tiles). Bitwise the same
+  // outputs in deterministic mode; measured within noise at cfg3 batch 1 r = 15 % and 1-1.5 % faster at
+  // r = 10 / 20 % (profiles/r02_ab_oproj_early.txt): the board is at its power cap, so the overlapped
+  // O-proj mostly trades clock for concurrency. Off by default.
+  static const bool early_env = [] { const char* e = std::getenv("RC_OPROJ_EARLY"); return e && std::atoi(e) == 1; }();
+  const bool early = early_env && c->early_on && !paired && c->attn_tc && n_splits == 1 && rows <= 1024 &&
+                     !at.lse_out && gemm_use_transposed(rows, d, EPI_ADD_F32, dh, c->num_sms);
+  if (early) at.ready = c->oproj_ready;
   if (paired)
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending,
               attn_pair_launch(&c->mQ3, &c->mK_att[l], &c->mV_att[l], at, c->pd.arena_rows, s));
@@ -1175,6 +1192,10 @@ rc_status run_rest(rc_ctx* c, int l, float* x, const CUtensorMap* mx, int32_t ro
     RC_LAUNCH(RC_K_ATTN, attn_flops, 0, attn_pending, attn_launch(at, s));
   EpiArgs eo = epi_base(c);
   eo.out = x; eo.ldo = d; eo.det = det;
+  if (early) {
+    eo.ready = c->oproj_ready;
+    for (int i = 0; i < 4; ++i) eo.ready_tgt[i] = c->early_cnt[i] * Hk;
+  }
   RC_LAUNCH(RC_K_GEMM, gemm_flops(R, d, H * dh), gemm_bytes(R, d, H * dh, 8), -1,
             gemm_launch(&c->mA_o, &c->mB_o[l], mx, rows, d, H * dh, c->bn_o, EPI_ADD_F32, eo, c->num_sms, s,
                         &c->mA_o64));
@@ -1506,6 +1527,23 @@ rc_status rc_selective_prefill(rc_ctx* c, int32_t n_req, const rc_seq* seqs, con
   }
   const int Hq = m.n_heads * m.head_dim;  // q row width (bf16), moved as Hq / 2 four-byte words
   int32_t cur = S0;
+  // early O-projection over the final Sel list (one tile list for every selective layer, unsplit, not
+  // paired, <= 4 token tiles of 256 rows): attention CTAs per token tile
+  struct EarlyGuard { rc_ctx* c; ~EarlyGuard() { c->early_on = false; } } early_guard{c};
+  c->early_on = false;
+  if (G == 0 && split_s == 1 && !pair_s && S0 <= 1024) {
+    bool ok = true;
+    for (int i = 0; i < 4; ++i) c->early_cnt[i] = 0;
+    for (int i = 0; i < n_st; ++i) {
+      const int4 t = hst[i];
+      if (t.y <= 0) continue;
+      for (int tt = t.x / 256; tt <= (t.x + t.y - 1) / 256; ++tt) {
+        if (tt >= 4) ok = false;
+        else ++c->early_cnt[tt];
+      }
+    }
+    c->early_on = ok;
+  }
   for (int l = cL; l < L; ++l) {
     const int i = l - cL;
     const int det = prm->deterministic ? 1 : 0;

@@ -94,6 +94,12 @@ struct EpiArgs {
   int* ws_cnt = nullptr;    // 2 * gemm_ws_slots()
   int32_t ws_slots = 0;
   int32_t det = 1;          // 0: partial tiles reduce-add straight into x in arrival order
+  // transposed residual GEMM only (early O-projection): ready[tt] counts the attention CTAs done with
+  // 256-row token tile tt; a unit waits for ready[tt] >= ready_tgt[tt] (acquire) before loading its
+  // tokens instead of waiting for the whole attention grid (griddepcontrol.wait is skipped). ready[4]
+  // counts finished GEMM CTAs; the last one zeroes ready[0..4] for the next layer
+  int32_t* ready = nullptr;
+  int32_t ready_tgt[4] = {0, 0, 0, 0};
   int32_t t_pack = 0;       // transposed kernel: two stripes' 128-token tails share a slot (RC_GEMM_T_PACK)
   int32_t no_epi = 0;       // diagnostics: transposed kernel skips its epilogue (RC_GEMM_NOEPI)
 };
@@ -196,6 +202,9 @@ struct AttnArgs {
   unsigned long long* prof = nullptr;  // paired kernel phase timing (-DRC_ATTN_PROF builds, RC_ATTN_PROF=1)
   int32_t s_prefetch = 0;  // single-tile kernel: load S_{j+1} from TMEM before signalling P_j (RC_ATTN_SPREFETCH)
   VSrc vsrc;                      // zero-copy V: V rows through vmap (cp.async loads) instead of TMA boxes
+  // single-tile kernel, unsplit: per 256-row token tile, +1 per (tile, kv head) CTA whose output rows
+  // touch it, after they are written (early O-projection; EpiArgs::ready)
+  int32_t* ready = nullptr;
 };
 int attn_tokens_per_tile(int group);
 cudaError_t attn_launch(const AttnArgs& a, cudaStream_t s);

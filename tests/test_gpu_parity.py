@@ -609,3 +609,40 @@ def test_semlib_feeds_assemble_on_device():
             assert np.array_equal(G.bits(k)[m], K[l][m]) and np.array_equal(G.bits(v)[m], V[l][m]), (r, l)
     ctx.release(seqs)
     ctx.close()
+
+
+def _early_child(path, n_req):
+    G = _gpu()
+    wl = rcgen.MINI_L
+    case = make_case(wl, n_req=n_req)
+    pools = oracle_pools(case)
+    n_tok = sum(l.n for l in layouts(case))
+    ctx, _ = G.make_ctx(case, pools, n_tok)
+    lays = G.gpu_layouts(ctx, case)
+    seqs = ctx.assemble(lays, prefix_id=G.PREFIX_ID, gather_from=1)
+    n_cand = sum(len(l["cand_idtok"]) for l in lays)
+    out = ctx.selective_prefill(seqs, 1500, 1500, check_layer=1, hidden=True, n_cand=n_cand, deterministic=True)
+    torch.cuda.synchronize()
+    np.savez(path, logits=out["logits"].cpu().numpy(), hidden=out["hidden"].cpu().numpy(),
+             sel_pos=out["sel_pos"].cpu().numpy())
+    ctx.release(seqs)
+    ctx.close()
+
+
+@pytest.mark.parametrize("n_req", [1, 2])
+def test_early_oproj_is_bitwise_the_grid_wait(n_req, tmp_path):
+    """Early O-projection (the transposed O-proj waits per 256-row token tile for the attention CTAs that
+    write it, RC_OPROJ_EARLY=1, opt-in) against waiting for the whole attention grid (=0): the same
+    arithmetic in another schedule, so with deterministic residual sums the outputs are bitwise equal
+    (two requests: attention tiles straddle token-tile boundaries)."""
+    import subprocess, sys, os
+    outs = []
+    for ea in ("1", "0"):
+        path = str(tmp_path / f"early{ea}.npz")
+        code = ("import sys; sys.path.insert(0, %r); from tests.test_gpu_parity import _early_child; _early_child(%r, %d)"
+                % (os.getcwd(), path, n_req))
+        subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, RC_OPROJ_EARLY=ea), timeout=600)
+        outs.append(np.load(path))
+    a, b = outs
+    assert np.array_equal(a["sel_pos"], b["sel_pos"])
+    assert np.array_equal(a["logits"], b["logits"]) and np.array_equal(a["hidden"], b["hidden"])
