@@ -40,7 +40,10 @@ constexpr uint32_t SMEM_BYTES = OFF_FLAG + 16;
 constexpr uint32_t O_COL = 256;            // O_h at 256 + 128 h
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 domain
 // every 2^x of P on the SFU: measured at cfg3 batch 1, 1.49 ms per step vs 1.62 with 3/8 on the FMA pipe
-constexpr unsigned POLY_CHUNKS = 0x00;
+#ifndef RC_TC_POLY  // diagnostics builds only (RC_BUILD_DEFS=-DRC_TC_POLY=...): 8-key chunks on the FMA pipe
+#define RC_TC_POLY 0x00
+#endif
+constexpr unsigned POLY_CHUNKS = RC_TC_POLY;
 constexpr float SPEC_SUM_MAX = 18446744073709551616.0f;  // 2^64: bound of the speculative exps' row sum
 
 __global__ void __launch_bounds__(NTHREADS, 1)
